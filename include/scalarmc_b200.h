@@ -1,0 +1,283 @@
+/*
+ * scalarmc_b200.h — C ABI of the B200-native particle forward map G(u).
+ *
+ * This is the drop-in boundary for the reference library `scalarmc`
+ * (/root/reference/proj, arXiv 1808.10580).  Every entry point below replaces
+ * one reference C++ function on the hot path; the reference symbol it stands
+ * in for is cited next to it (paths relative to /root/reference/proj).  The C++
+ * shim in paper_1808_10580_b200/host/scalarmc_forward_gpu.cpp re-implements the
+ * unchanged C++ signatures (`observe_ad`, `observe_ad_single`, `observe_bvp`)
+ * on top of these calls, and the Python mirror (paper_1808_10580_b200/api.py)
+ * binds them with ctypes.
+ *
+ * Conventions
+ *   - Plain C types only: caller-owned POD inputs, caller-owned output arrays.
+ *   - Every function returns an smc_status; on failure smc_last_error() returns
+ *     a thread-local message.  The status maps 1:1 onto the exception type the
+ *     reference throws for the same condition (invalid_argument, out_of_range,
+ *     runtime_error), and the message text matches the reference's.
+ *   - Calls are synchronous: they return once host outputs are written.
+ *   - There is no CPU fallback: without a CUDA device smc_create fails.
+ */
+#ifndef SCALARMC_B200_H
+#define SCALARMC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Every declaration below is exported even when the library is built with
+ * -fvisibility=hidden. */
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define SMC_ABI_VERSION 1
+
+/* Status codes; the comment names the reference exception type. */
+typedef enum smc_status {
+    SMC_OK = 0,
+    SMC_EINVAL = 1,   /* std::invalid_argument */
+    SMC_ERANGE = 2,   /* std::out_of_range */
+    SMC_ERUNTIME = 3, /* std::runtime_error (all particles failed, ...) */
+    SMC_ECUDA = 4     /* CUDA / device failure (no reference analogue) */
+} smc_status;
+
+/* ParticleEstimate (include/scalarmc/executor.hpp:13-19), same field order. */
+typedef struct smc_estimate {
+    double mean;
+    double std_error;
+    int64_t n_particles;
+    int64_t n_failed;
+    double aux_mean;
+} smc_estimate;
+
+/* ScalarField (include/scalarmc/fields.hpp:121-164; eval src/fields.cpp:235-253).
+ * kind: 0 constant, 1 cosine series, 2 Gaussian bumps, 3 linear (affine).
+ * Arrays are SoA with n_terms entries; unused pointers may be NULL. */
+typedef enum smc_scalar_kind {
+    SMC_SCALAR_CONSTANT = 0,
+    SMC_SCALAR_COSINE = 1,
+    SMC_SCALAR_BUMPS = 2,
+    SMC_SCALAR_LINEAR = 3
+} smc_scalar_kind;
+
+typedef struct smc_scalar_field {
+    int32_t kind;
+    int32_t n_terms;
+    double constant;        /* constant value, or affine offset */
+    double gradient[2];     /* linear: gradient */
+    double sharpness;       /* bumps: a in exp(-a |x-c|^2) */
+    const double* amplitude;/* cosine/bumps: [n_terms] */
+    const double* freq;     /* cosine: [n_terms][2] angular frequency (2 pi k for torus modes) */
+    const double* phase;    /* cosine: [n_terms] */
+    const double* center;   /* bumps: [n_terms][2] */
+} smc_scalar_field;
+
+/* VelocityField (include/scalarmc/fields.hpp:67-86): constant vector or a
+ * FourierVelocityField (fields.hpp:24-64).  Modes are given as the caller holds
+ * them (any sign convention); the library canonicalises and sorts exactly like
+ * the reference constructor (src/fields.cpp:35-69). */
+typedef struct smc_velocity {
+    int32_t is_constant;
+    int32_t max_wavenumber; /* K, > 0 for Fourier fields */
+    double constant[2];
+    int64_t n_modes;
+    const int32_t* k;       /* [n_modes][2] (k1, k2) */
+    const double* coeff;    /* [n_modes][2] (re, im) */
+} smc_velocity;
+
+typedef enum smc_scheme { SMC_EULER_MARUYAMA = 0, SMC_MILSTEIN = 1 } smc_scheme;
+
+/* Precision of the particle kernels.  FP64 is the parity path (1e-10 relative
+ * gate); FP32 is the optional fast mode (3 Monte Carlo SE gate). STRICT is the
+ * FP64 diagnostic build that keeps the reference's operation order and does no
+ * FMA contraction. */
+typedef enum smc_precision { SMC_FP64 = 0, SMC_FP32 = 1, SMC_FP64_STRICT = 2 } smc_precision;
+
+/* AdProblemSpec (include/scalarmc/forward_ad.hpp:23-34).  The diffusion is the
+ * isotropic model sigma = sqrt(2 kappa) (fields.cpp:158-165); diagonal
+ * std::function models have no device representation and are rejected by the
+ * C++ shim with std::invalid_argument. */
+typedef struct smc_ad_problem {
+    smc_velocity velocity;
+    double kappa;
+    smc_scalar_field initial_condition;
+    int64_t n_obs;
+    const double* obs_t;    /* [n_obs] */
+    const double* obs_x;    /* [n_obs][2] */
+    double dt;              /* <= 0: min_j t_j / 200 (forward_ad.cpp:10-15) */
+    int64_t n_particles;
+    int32_t scheme;         /* smc_scheme; Milstein == EM for isotropic sigma (sde.cpp:21) */
+    int32_t precision;      /* smc_precision */
+} smc_ad_problem;
+
+/* Domain (include/scalarmc/geometry.hpp:36-74). */
+typedef enum smc_domain_kind { SMC_DOMAIN_TORUS = 0, SMC_DOMAIN_BOX = 1, SMC_DOMAIN_DISK = 2 } smc_domain_kind;
+
+typedef struct smc_domain {
+    int32_t kind;
+    int32_t pad_;
+    double lower[2], upper[2];  /* box */
+    double center[2];           /* disk */
+    double radius;              /* disk */
+} smc_domain;
+
+/* BvpProblemSpec (include/scalarmc/forward_bvp.hpp:16-30). */
+typedef struct smc_bvp_problem {
+    smc_velocity velocity;
+    double kappa;
+    smc_scalar_field forcing;
+    smc_scalar_field boundary_data;
+    smc_domain domain;
+    int64_t n_obs;
+    const double* obs_x;    /* [n_obs][2] */
+    double dt;              /* <= 0: clipped default rule (forward_bvp.cpp:9-18) */
+    int64_t n_particles;
+    int32_t scheme;
+    int32_t precision;
+    int64_t max_steps;
+} smc_bvp_problem;
+
+/* PriorSpec (include/scalarmc/inference.hpp:22-38): fixes the u layout
+ * [Re, Im] per mode in |k|^2-then-(k1,k2) order (inference.cpp:24-40, :63-73). */
+typedef struct smc_prior {
+    int32_t cutoff;
+    int32_t pad_;
+    double s0;
+    double alpha;
+} smc_prior;
+
+/* ---- context ------------------------------------------------------------ */
+typedef struct smc_ctx smc_ctx;
+
+/* One context per process per GPU (torch.distributed launches one process per
+ * GPU).  Owns the stream and the persistent device buffers reused across calls
+ * (MCMC calls the forward map 1e5+ times). */
+smc_status smc_create(int device, smc_ctx** out);
+void smc_destroy(smc_ctx* ctx);
+const char* smc_last_error(void);
+int smc_abi_version(void);
+
+/* ---- forward maps (the drop-in boundary) --------------------------------- */
+
+/* observe_ad (include/scalarmc/forward_ad.hpp:39-40, src/forward_ad.cpp:53-60).
+ * out: [n_obs]. */
+smc_status smc_ad_observe(smc_ctx* ctx, const smc_ad_problem* prob, uint64_t seed,
+                          smc_estimate* out);
+
+/* observe_ad_single (forward_ad.hpp:43-44, forward_ad.cpp:62-69). */
+smc_status smc_ad_observe_single(smc_ctx* ctx, const smc_ad_problem* prob, uint64_t obs_index,
+                                 uint64_t seed, smc_estimate* out);
+
+/* Batched AD forward map: B parameter samples per launch.  u: [B][2M] in the
+ * prior's component order — each row is what velocity_from_coefficients
+ * (inference.cpp:63-73) turns into a field, so row b reproduces
+ * LikelihoodSpec::misfit's observe_ad call (inference.cpp:93-104) for u_b.
+ * seeds: [B], or NULL for common random numbers (every sample uses `seed`).
+ * The velocity slot of `base` is ignored. out: [B][n_obs]. */
+smc_status smc_ad_observe_batched(smc_ctx* ctx, const smc_ad_problem* base, const smc_prior* prior,
+                                  int64_t n_samples, const double* u, const uint64_t* seeds,
+                                  uint64_t seed, smc_estimate* out);
+
+/* observe_bvp (include/scalarmc/forward_bvp.hpp:35-36, src/forward_bvp.cpp:34-49).
+ * out: [n_obs]; aux_mean is the mean exit time. */
+smc_status smc_bvp_observe(smc_ctx* ctx, const smc_bvp_problem* prob, uint64_t seed,
+                           smc_estimate* out);
+
+/* ---- resolved step sizes (host only, no device needed) ------------------- */
+/* AdProblemSpec::resolved_dt (forward_ad.cpp:10-15). */
+smc_status smc_ad_resolved_dt(const smc_ad_problem* prob, double* out);
+/* BvpProblemSpec::resolved_dt (forward_bvp.cpp:9-18). */
+smc_status smc_bvp_resolved_dt(const smc_bvp_problem* prob, double* out);
+/* Validation only (forward_ad.cpp:17-28, forward_bvp.cpp:20-32). */
+smc_status smc_ad_validate(const smc_ad_problem* prob);
+smc_status smc_bvp_validate(const smc_bvp_problem* prob);
+/* FourierVelocityField constructor checks (fields.cpp:35-69). */
+smc_status smc_velocity_validate(const smc_velocity* v);
+/* sizeof of the ABI structs, in declaration order (estimate, scalar_field,
+ * velocity, ad_problem, domain, bvp_problem, prior, stats) — lets bindings
+ * check their layout.  Returns the number written. */
+int smc_struct_sizes(int64_t* out, int cap);
+
+/* ---- sharded / device-level API (multi-GPU, one process per GPU) ----------
+ * A forward map sharded over W ranks: particles of every observation are cut
+ * into aligned chunks of SMC_CHUNK particles; rank r simulates chunks
+ * [r*C/W, (r+1)*C/W).  Each rank produces exact aligned-tree partial sums per
+ * chunk (the reference's pairwise_sum tree restricted to the chunk,
+ * executor.cpp:11-26), the caller all-gathers them (NCCL), and every rank
+ * finishes the same tree — so the result is bit-identical for any W. */
+#define SMC_CHUNK 1024
+
+/* Number of chunks per observation for n_particles. */
+int64_t smc_num_chunks(int64_t n_particles);
+
+/* Simulate this rank's chunk range of every observation, then write the
+ * per-chunk value partials. partials_dev: device pointer [n_obs][n_chunks_local].
+ * The per-particle values stay in the context for smc_ad_shard_sq_partials. */
+smc_status smc_ad_shard_partials(smc_ctx* ctx, const smc_ad_problem* prob, uint64_t seed,
+                                 int64_t chunk_begin, int64_t chunk_end, double* partials_dev);
+
+/* Finish the tree over all chunks: partials_dev [n_obs][n_chunks] (device) ->
+ * sums_dev [n_obs] (device). */
+smc_status smc_tree_finish(smc_ctx* ctx, const double* partials_dev, int64_t n_obs,
+                           int64_t n_chunks, double* sums_dev);
+
+/* Second pass: chunk partials of (v - mean_j)^2 for the same chunk range.
+ * means_dev: [n_obs] device. */
+smc_status smc_ad_shard_sq_partials(smc_ctx* ctx, const double* means_dev, int64_t n_obs,
+                                    int64_t chunk_begin, int64_t chunk_end, double* partials_dev);
+
+/* Device stream the context launches on (cudaStream_t as void*).  A caller
+ * that already owns a stream (torch, NCCL) can hand it to the context so the
+ * forward map and the collectives are ordered on one stream; NULL restores the
+ * context's own stream. */
+void* smc_stream(smc_ctx* ctx);
+smc_status smc_set_stream(smc_ctx* ctx, void* stream);
+
+/* ---- diagnostics ---------------------------------------------------------- */
+/* Per-particle terminal values theta_0(X_T) for one observation, particles
+ * [0, n) (parity diagnostics). out: [n] host. */
+smc_status smc_ad_particle_values(smc_ctx* ctx, const smc_ad_problem* prob, uint64_t obs_index,
+                                   uint64_t seed, int64_t n, double* out);
+
+/* Per-walker (value, exit time, failed) for one BVP observation. */
+smc_status smc_bvp_particle_values(smc_ctx* ctx, const smc_bvp_problem* prob, uint64_t obs_index,
+                                   uint64_t seed, int64_t n, double* values, double* aux,
+                                   uint8_t* failed);
+
+/* Philox4x32-10 block and Box-Muller pair evaluated ON THE DEVICE for n
+ * (counter, key) inputs (rng.cpp:33-41, :53-72) — the KAT hook. */
+smc_status smc_philox_device(smc_ctx* ctx, int64_t n, const uint32_t* ctr, const uint32_t* key,
+                             uint32_t* out);
+smc_status smc_normal_pairs_device(smc_ctx* ctx, uint64_t seed, uint64_t obs, uint64_t particle,
+                                   int64_t n_blocks, double* out);
+
+/* Stats of the last forward-map call on this context: kernel time of the
+ * particle kernel (ms, CUDA events on the launching stream), its launch count,
+ * and the total particle-steps executed. */
+typedef struct smc_stats {
+    double particle_kernel_ms;
+    double reduce_ms;
+    int64_t kernel_launches;   /* this call */
+    int64_t particle_steps;
+    int64_t total_launches;    /* cumulative over the context's life */
+} smc_stats;
+smc_status smc_last_stats(smc_ctx* ctx, smc_stats* out);
+
+/* FP64 DFMA peak microbenchmark (roofline denominator): runs a DFMA-only
+ * kernel over all SMs for about `ms` milliseconds; returns TFLOP/s. */
+smc_status smc_fp64_peak(smc_ctx* ctx, double ms, double* tflops);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SCALARMC_B200_H */

@@ -1,0 +1,251 @@
+"""ctypes bindings of the parity checkers (TEST INFRASTRUCTURE ONLY).
+
+Two CPU checkers share the C-ABI POD structs of include/scalarmc_b200.h:
+
+  Port       oracle/liboracle.so — the plain-C restatement (scalarmc_oracle.c)
+  Reference  oracle/_ref/libscalarmc_ref.so — the real reference scalarmc,
+             compiled from /root/reference/proj/src (oracle/Makefile) behind
+             the extern "C" harness ref_capi.cpp
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline and
+--impl reference) import this module, and only to check or time the
+reference — never as the product path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+from paper_1808_10580_b200 import _abi as A
+
+HERE = Path(__file__).resolve().parent
+PORT_LIB = HERE / "liboracle.so"
+REF_LIB = HERE / "_ref" / "libscalarmc_ref.so"
+
+_dp = C.POINTER(C.c_double)
+_u32p = C.POINTER(C.c_uint32)
+_i32p = C.POINTER(C.c_int32)
+_i64p = C.POINTER(C.c_int64)
+_u8p = C.POINTER(C.c_uint8)
+
+
+def _status(lib, prefix: str, rc: int) -> None:
+    if rc == 0:
+        return
+    msg = getattr(lib, prefix + "last_error")().decode()
+    if rc == A.SMC_EINVAL:
+        raise ValueError(msg)
+    if rc == A.SMC_ERANGE:
+        raise IndexError(msg)
+    raise RuntimeError(msg)
+
+
+class _Checker:
+    prefix = ""
+    takes_workers = False
+
+    def __init__(self, path: Path):
+        if not path.exists():
+            raise FileNotFoundError(f"{path} not built (make -C oracle)")
+        self.lib = C.CDLL(str(path))
+        L, P = self.lib, self.prefix
+        getattr(L, P + "last_error").restype = C.c_char_p
+        getattr(L, P + "pairwise_sum").restype = C.c_double
+        getattr(L, P + "pairwise_sum").argtypes = [_dp, C.c_int64]
+        for name in ("stream_draws", "prior_modes", "prior_draw"):
+            getattr(L, P + name).restype = C.c_int64
+
+    def _f(self, name):
+        return getattr(self.lib, self.prefix + name)
+
+    def _w(self, workers):
+        return (C.c_int(workers),) if self.takes_workers else ()
+
+    # -- rng ----------------------------------------------------------------
+    def philox(self, ctr, key) -> np.ndarray:
+        ctr = np.ascontiguousarray(ctr, dtype=np.uint32).reshape(-1, 4)
+        key = np.ascontiguousarray(key, dtype=np.uint32).reshape(-1, 2)
+        out = np.empty_like(ctr)
+        f = self._f("philox4x32")
+        for i in range(ctr.shape[0]):
+            f(ctr[i].ctypes.data_as(_u32p), key[i].ctypes.data_as(_u32p), out[i].ctypes.data_as(_u32p))
+        return out
+
+    def normal_pairs(self, seed: int, obs: int, particle: int, n: int) -> np.ndarray:
+        out = np.empty((n, 2), dtype=np.float64)
+        self._f("normal_pairs")(C.c_uint64(seed), C.c_uint64(obs) if self.takes_workers else C.c_uint32(obs),
+                                C.c_uint64(particle) if self.takes_workers else C.c_uint32(particle),
+                                C.c_int64(n), out.ctypes.data_as(_dp))
+        return out
+
+    def stream_draws(self, seed: int, obs: int, particle: int, ops) -> np.ndarray:
+        ops = np.ascontiguousarray(ops, dtype=np.int32)
+        out = np.empty(2 * len(ops), dtype=np.float64)
+        conv = C.c_uint64 if self.takes_workers else C.c_uint32
+        w = self._f("stream_draws")(C.c_uint64(seed), conv(obs), conv(particle), C.c_int64(len(ops)),
+                                    ops.ctypes.data_as(_i32p), out.ctypes.data_as(_dp))
+        return out[:w]
+
+    # -- fields -------------------------------------------------------------
+    def velocity_eval(self, velocity, x) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1, 2)
+        out = np.empty_like(x)
+        pod = velocity._pod()
+        _status(self.lib, self.prefix, self._f("velocity_eval")(C.byref(pod), C.c_int64(x.shape[0]),
+                                                                 x.ctypes.data_as(_dp), out.ctypes.data_as(_dp)))
+        return out
+
+    def scalar_eval(self, field, x) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1, 2)
+        out = np.empty(x.shape[0], dtype=np.float64)
+        pod = field._pod()
+        rc = self._f("scalar_eval")(C.byref(pod), C.c_int64(x.shape[0]), x.ctypes.data_as(_dp),
+                                    out.ctypes.data_as(_dp))
+        if self.takes_workers:
+            _status(self.lib, self.prefix, rc)
+        return out
+
+    def pairwise_sum(self, values) -> float:
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        return self._f("pairwise_sum")(v.ctypes.data_as(_dp), C.c_int64(v.size))
+
+    # -- forward maps -------------------------------------------------------
+    def observe_ad(self, spec, seed: int, workers: int = 0) -> np.ndarray:
+        p, keep = spec._pod()
+        out = np.zeros(p.n_obs, dtype=_est_dtype())
+        rc = self._f("ad_observe")(C.byref(p), C.c_uint64(seed), *self._w(workers),
+                                   out.ctypes.data_as(C.POINTER(A.smc_estimate)))
+        _status(self.lib, self.prefix, rc)
+        return out
+
+    def ad_particle_values(self, spec, obs_index: int, seed: int, n: int, terminal: bool = False):
+        p, keep = spec._pod()
+        out = np.empty(n, dtype=np.float64)
+        term = np.empty((n, 2), dtype=np.float64) if terminal else None
+        rc = self._f("ad_particle_values")(C.byref(p), C.c_uint64(obs_index), C.c_uint64(seed), C.c_int64(n),
+                                           out.ctypes.data_as(_dp), term.ctypes.data_as(_dp) if terminal else _dp())
+        _status(self.lib, self.prefix, rc)
+        return (out, term) if terminal else out
+
+    def observe_bvp(self, spec, seed: int, workers: int = 0) -> np.ndarray:
+        p, keep = spec._pod()
+        out = np.zeros(p.n_obs, dtype=_est_dtype())
+        rc = self._f("bvp_observe")(C.byref(p), C.c_uint64(seed), *self._w(workers),
+                                    out.ctypes.data_as(C.POINTER(A.smc_estimate)))
+        _status(self.lib, self.prefix, rc)
+        return out
+
+    def bvp_particle_values(self, spec, obs_index: int, seed: int, n: int):
+        p, keep = spec._pod()
+        vals = np.empty(n, dtype=np.float64)
+        aux = np.empty(n, dtype=np.float64)
+        failed = np.empty(n, dtype=np.uint8)
+        steps = np.empty(n, dtype=np.int64)
+        rc = self._f("bvp_particle_values")(C.byref(p), C.c_uint64(obs_index), C.c_uint64(seed), C.c_int64(n),
+                                            vals.ctypes.data_as(_dp), aux.ctypes.data_as(_dp),
+                                            failed.ctypes.data_as(_u8p), steps.ctypes.data_as(_i64p))
+        _status(self.lib, self.prefix, rc)
+        return vals, aux, failed, steps
+
+    # -- u -> field ---------------------------------------------------------
+    def prior_modes(self, cutoff: int) -> np.ndarray:
+        cap = 4 * (cutoff + 1) ** 2
+        out = np.empty((cap, 2), dtype=np.int32)
+        n = self._f("prior_modes")(C.c_int(cutoff), out.ctypes.data_as(_i32p), C.c_int64(cap))
+        return out[:n].copy()
+
+    def prior_draw(self, prior, seed: int, obs: int, particle: int) -> np.ndarray:
+        cap = 8 * (prior.cutoff + 1) ** 2
+        out = np.empty(cap, dtype=np.float64)
+        n = self._f("prior_draw")(C.byref(prior._pod()), C.c_uint64(seed), C.c_uint64(obs), C.c_uint64(particle),
+                                  out.ctypes.data_as(_dp), C.c_int64(cap))
+        return out[:n].copy()
+
+
+def _est_dtype():
+    return np.dtype([("mean", "<f8"), ("std_error", "<f8"), ("n_particles", "<i8"), ("n_failed", "<i8"),
+                     ("aux_mean", "<f8")])
+
+
+class Port(_Checker):
+    """The plain-C restatement (oracle/scalarmc_oracle.c)."""
+    prefix = "orc_"
+    takes_workers = False
+
+    def __init__(self, path: Path = PORT_LIB):
+        super().__init__(path)
+        self.lib.orc_bvp_resolved_dt.restype = C.c_double
+
+
+class Reference(_Checker):
+    """The real reference library compiled from /root/reference sources."""
+    prefix = "ref_"
+    takes_workers = True
+
+    def __init__(self, path: Path = REF_LIB):
+        super().__init__(path)
+        self.lib.ref_resolve_workers.restype = C.c_int
+
+    def resolve_workers(self, n: int = 0) -> int:
+        return self.lib.ref_resolve_workers(n)
+
+    def observe_ad_single(self, spec, obs_index: int, seed: int, workers: int = 0):
+        p, keep = spec._pod()
+        out = np.zeros(1, dtype=_est_dtype())
+        rc = self.lib.ref_ad_observe_single(C.byref(p), C.c_uint64(obs_index), C.c_uint64(seed), C.c_int(workers),
+                                            out.ctypes.data_as(C.POINTER(A.smc_estimate)))
+        _status(self.lib, self.prefix, rc)
+        return out[0]
+
+    def observe_ad_u(self, spec, prior, u, seed: int, workers: int = 0) -> np.ndarray:
+        p, keep = spec._pod()
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        out = np.zeros(p.n_obs, dtype=_est_dtype())
+        rc = self.lib.ref_ad_observe_u(C.byref(p), C.byref(prior._pod()), u.ctypes.data_as(_dp), C.c_uint64(seed),
+                                       C.c_int(workers), out.ctypes.data_as(C.POINTER(A.smc_estimate)))
+        _status(self.lib, self.prefix, rc)
+        return out
+
+    def misfit(self, spec, prior, u, data, noise_std: float, forward_seed: int, workers: int = 0) -> float:
+        p, keep = spec._pod()
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        d = np.ascontiguousarray(data, dtype=np.float64)
+        out = C.c_double()
+        rc = self.lib.ref_misfit(C.byref(p), C.byref(prior._pod()), u.ctypes.data_as(_dp), d.ctypes.data_as(_dp),
+                                 C.c_double(noise_std), C.c_uint64(forward_seed), C.c_int(workers), C.byref(out))
+        _status(self.lib, self.prefix, rc)
+        return out.value
+
+    def forcing_cost(self, spec, amplitudes, centers, sharpness: float, target, seed: int, workers: int = 0) -> float:
+        p, keep = spec._pod()
+        a = np.ascontiguousarray(amplitudes, dtype=np.float64)
+        c = np.ascontiguousarray(centers, dtype=np.float64).reshape(-1, 2)
+        t = np.ascontiguousarray(target, dtype=np.float64)
+        out = C.c_double()
+        rc = self.lib.ref_forcing_cost(C.byref(p), C.c_int64(a.size), a.ctypes.data_as(_dp), c.ctypes.data_as(_dp),
+                                       C.c_double(sharpness), t.ctypes.data_as(_dp), C.c_uint64(seed),
+                                       C.c_int(workers), C.byref(out))
+        _status(self.lib, self.prefix, rc)
+        return out.value
+
+    def resolved_dt_ad(self, spec) -> float:
+        p, keep = spec._pod()
+        out = C.c_double()
+        _status(self.lib, self.prefix, self.lib.ref_ad_resolved_dt(C.byref(p), C.byref(out)))
+        return out.value
+
+    def resolved_dt_bvp(self, spec) -> float:
+        p, keep = spec._pod()
+        out = C.c_double()
+        _status(self.lib, self.prefix, self.lib.ref_bvp_resolved_dt(C.byref(p), C.byref(out)))
+        return out.value
+
+
+def port_available() -> bool:
+    return PORT_LIB.exists()
+
+
+def reference_available() -> bool:
+    return REF_LIB.exists()

@@ -1,0 +1,44 @@
+"""scalarmc_b200 — B200-native particle forward map G(u) of arXiv 1808.10580.
+
+Drop-in for the hot path of the reference library scalarmc: observe_ad /
+observe_ad_single / observe_bvp (and the u -> G callers misfit / forcing_cost)
+run as fused sm_100a kernels behind the C ABI in include/scalarmc_b200.h.
+"""
+from .api import (  # noqa: F401
+    AdObservation,
+    AdProblemSpec,
+    Bump,
+    BvpProblemSpec,
+    Context,
+    CosineTerm,
+    DiffusionModel,
+    Domain,
+    ESTIMATE_DTYPE,
+    ForcingControl,
+    FourierVelocityField,
+    LikelihoodSpec,
+    ParticleEstimate,
+    Point2,
+    Precision,
+    PriorSpec,
+    ScalarField,
+    StepScheme,
+    Vec2,
+    VelocityField,
+    VelocityMode,
+    ad_particle_values,
+    bvp_particle_values,
+    default_context,
+    forcing_cost,
+    normal_pairs_device,
+    observe_ad,
+    observe_ad_batched,
+    observe_ad_single,
+    observe_bvp,
+    philox_device,
+    prior_draw,
+    velocity_from_coefficients,
+)
+from ._abi import LIB_PATH, load_library  # noqa: F401
+
+__version__ = "0.1.0"

@@ -1,0 +1,134 @@
+// bvp_body.cuh — K2 exit-time walker kernel body (Algorithm 2).
+//
+// Per walker (forward_bvp.cpp:39-46 -> simulate_to_exit, sde.cpp:52-77):
+//   loop step < max_steps:
+//     next = x - v(x) dt + sigma sqrt(dt) xi            (em_step, sde.cpp:8-16)
+//     if next leaves D: exit point by segment crossing (geometry.cpp:56-114),
+//        f_int += f(x) frac dt, tau = step dt + frac dt, value = bc(exit) - f_int
+//     else f_int += f(x) dt, x = next
+//   failed (value 0, excluded) after max_steps.
+//
+// Exit times are heavy-tailed, so walkers are not pinned to threads: each warp
+// is persistent and refills lanes whose walker finished from a global queue
+// (ballot -> one atomicAdd per refill -> rank by popc), keeping all 32 lanes
+// busy until the queue drains.  Every walker's randomness is addressed by
+// (seed, obs, particle, step), so refill order never changes results.
+//
+// Included by bvp_kernels.cu (FMA contraction on; FP64 + FP32) and
+// bvp_strict.cu (-fmad=false; the reference's operation order).
+#pragma once
+
+#include "kernels.h"
+#include "scalar_eval.cuh"
+#include "smc_device.cuh"
+#include "velocity.cuh"
+
+namespace smc {
+
+constexpr int kBvpBlock = 128;
+
+template <class T, bool STRICT, int KCAP>
+__global__ void __launch_bounds__(kBvpBlock) bvp_walkers(const BvpLaunch L) {
+    constexpr unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned long long total = static_cast<unsigned long long>(L.n_obs) * L.n_particles;
+    const uint32_t k0 = static_cast<uint32_t>(L.seed), k1 = static_cast<uint32_t>(L.seed >> 32);
+    const LatticeImg& lat = L.vel.lat;
+    const T dt = T(L.dt), sr = T(L.sr);
+
+    bool active = false, exhausted = false;
+    unsigned long long w = 0;
+    uint32_t obs = 0, particle = 0;
+    int64_t step = 0;
+    T x1 = T(0), x2 = T(0), f_int = T(0);
+    unsigned long long my_steps = 0;
+    cd p1[STRICT ? KCAP + 1 : 1], p2[STRICT ? KCAP + 1 : 1];
+
+    for (;;) {
+        if (!exhausted) {
+            const unsigned need = __ballot_sync(FULL, !active);
+            if (need) {
+                const int leader = __ffs(need) - 1;
+                unsigned long long base = 0;
+                if (lane == leader) base = atomicAdd(L.counter, static_cast<unsigned long long>(__popc(need)));
+                base = __shfl_sync(FULL, base, leader);
+                if (base + __popc(need) >= total) exhausted = true;
+                if (!active) {
+                    const unsigned long long idx = base + __popc(need & ((1u << lane) - 1u));
+                    if (idx < total) {
+                        w = idx;
+                        obs = static_cast<uint32_t>(idx / static_cast<unsigned long long>(L.n_particles));
+                        particle = static_cast<uint32_t>(idx - static_cast<unsigned long long>(obs) * L.n_particles);
+                        x1 = T(__ldg(L.obs_x + 2 * obs));
+                        x2 = T(__ldg(L.obs_x + 2 * obs + 1));
+                        f_int = T(0);
+                        step = 0;
+                        active = true;
+                    }
+                }
+            }
+        }
+        if (!__any_sync(FULL, active)) break;
+        if (active) {
+            const Uniform2 u = uniform_block(k0, k1, L.obs_slot0 + obs, particle, static_cast<uint64_t>(step));
+            T xi1, xi2, v1, v2;
+            if constexpr (STRICT) {
+                const double r = sqrt(-2.0 * log(u.u0));
+                const double a = 2.0 * kPi * u.u1;
+                xi1 = r * cos(a);
+                xi2 = r * sin(a);
+                velocity_strict<KCAP>(L.vel, p1, p2, x1, x2, v1, v2);
+            } else {
+                const T rad = sqrt(T(-2) * log(T(u.u0)));
+                T sn, cs;
+                sincospi_t(T(2) * T(u.u1), &sn, &cs);
+                xi1 = rad * cs;
+                xi2 = rad * sn;
+                if (L.vel.is_constant) {
+                    v1 = T(L.vel.c1);
+                    v2 = T(L.vel.c2);
+                } else {
+                    velocity_lattice<T>(lat, lat.coef, lat.row0, lat.g0, x1, x2, v1, v2);
+                }
+            }
+            T n1, n2;
+            if constexpr (STRICT) {
+                n1 = x1 - v1 * L.dt + L.sigma * L.root_dt * xi1;
+                n2 = x2 - v2 * L.dt + L.sigma * L.root_dt * xi2;
+            } else {
+                n1 = fma(sr, xi1, fma(-v1, dt, x1));
+                n2 = fma(sr, xi2, fma(-v2, dt, x2));
+            }
+            const T f = T(scalar_eval(L.forcing, double(x1), double(x2)));
+            ++my_steps;
+            if (!domain_contains<T>(L.domain, n1, n2)) {
+                T h1, h2;
+                const T frac = boundary_exit<T>(L.domain, x1, x2, n1, n2, h1, h2);
+                f_int += f * frac * dt;
+                const T tau = T(double(step)) * dt + frac * dt;
+                L.values[w] = scalar_eval(L.boundary, double(h1), double(h2)) - double(f_int);
+                L.aux[w] = double(tau);
+                L.failed[w] = 0;
+                active = false;
+            } else {
+                f_int += f * dt;
+                x1 = n1;
+                x2 = n2;
+                ++step;
+                if (step >= L.max_steps) {
+                    L.values[w] = 0.0;
+                    L.aux[w] = 0.0;
+                    L.failed[w] = 1;
+                    active = false;
+                }
+            }
+        }
+    }
+    // one atomic per warp for the walker-step count
+    unsigned long long s = my_steps;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(FULL, s, off);
+    if (lane == 0 && s) atomicAdd(L.step_total, s);
+}
+
+}  // namespace smc

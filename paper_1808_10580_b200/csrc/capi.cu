@@ -1,0 +1,806 @@
+// capi.cu — the C ABI (include/scalarmc_b200.h): context, device-image
+// upload, kernel orchestration and host result return.
+//
+// One smc_ctx per process per GPU.  A forward-map call is: validate (host, the
+// reference's messages) -> pack one image (velocity lattice, theta_0 terms,
+// per-observation step schedules) into pinned staging -> one H2D copy -> K1
+// particle kernel -> K3 tree reduction passes -> estimates kernel -> one D2H
+// copy of n_obs x 40 B.  All on the context's stream; persistent buffers grow
+// and are reused across calls.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/scalarmc_b200.h"
+#include "host_problem.h"
+#include "kernels.h"
+
+using namespace smc;
+
+namespace {
+
+thread_local std::string g_err;
+
+#define CK(x)                                                                                       \
+    do {                                                                                            \
+        cudaError_t e_ = (x);                                                                       \
+        if (e_ != cudaSuccess) raise(SMC_ECUDA, std::string("CUDA error: ") + cudaGetErrorString(e_) + \
+                                                    " (" #x ")");                                   \
+    } while (0)
+
+template <class F>
+smc_status guarded(F&& f) {
+    try {
+        f();
+        return SMC_OK;
+    } catch (const Error& e) {
+        g_err = e.msg;
+        return static_cast<smc_status>(e.code);
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return SMC_ERUNTIME;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return SMC_ERUNTIME;
+    }
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    template <class T>
+    T* get(size_t n) {
+        const size_t bytes = std::max<size_t>(n * sizeof(T), 16);
+        if (bytes > cap) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            cap = 0;
+            CK(cudaMalloc(&p, bytes));
+            cap = bytes;
+        }
+        return static_cast<T*>(p);
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+struct PinnedBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    template <class T>
+    T* get(size_t n) {
+        const size_t bytes = std::max<size_t>(n * sizeof(T), 16);
+        if (bytes > cap) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            cap = 0;
+            CK(cudaMallocHost(&p, bytes));
+            cap = bytes;
+        }
+        return static_cast<T*>(p);
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+// Host-side image under construction: 16-byte aligned blobs in one arena.
+struct Image {
+    std::vector<unsigned char> bytes;
+    size_t add(const void* src, size_t n) {
+        const size_t off = (bytes.size() + 15) & ~size_t(15);
+        bytes.resize(off + std::max<size_t>(n, 1));
+        if (n) std::memcpy(bytes.data() + off, src, n);
+        return off;
+    }
+    template <class T>
+    size_t add_vec(const std::vector<T>& v) {
+        return add(v.data(), v.size() * sizeof(T));
+    }
+    size_t reserve(size_t n) {
+        const size_t off = (bytes.size() + 15) & ~size_t(15);
+        bytes.resize(off + std::max<size_t>(n, 1));
+        return off;
+    }
+};
+
+}  // namespace
+
+struct smc_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;      // stream every launch goes to
+    cudaStream_t own_stream = nullptr;  // the context's own stream
+    int64_t total_launches = 0;
+    cudaEvent_t ev[4] = {};
+    DevBuf image, values, aux, flags, flags2, scratch, sums, means, sumsq, sumaux, est, counts, tmp_a, tmp_b, tmp_c;
+    PinnedBuf staging, est_host;
+    smc_stats stats{};
+    // sharded AD state (smc_ad_shard_*)
+    int64_t shard_n_obs = 0, shard_span = 0;
+
+    unsigned char* upload(const Image& img) {
+        unsigned char* h = staging.get<unsigned char>(img.bytes.size());
+        std::memcpy(h, img.bytes.data(), img.bytes.size());
+        unsigned char* d = image.get<unsigned char>(img.bytes.size());
+        CK(cudaMemcpyAsync(d, h, img.bytes.size(), cudaMemcpyHostToDevice, stream));
+        return d;
+    }
+};
+
+namespace {
+
+void count_launches(smc_ctx* ctx, int64_t n) {
+    ctx->stats.kernel_launches += n;
+    ctx->total_launches += n;
+}
+
+// ScalarField image: term arrays appended to the image; pointers patched
+// after upload.
+struct ScalarRef {
+    ScalarImg img{};
+    size_t amp = 0, freq = 0, phase = 0, center = 0;
+};
+
+ScalarRef add_scalar(Image& im, const smc_scalar_field& f) {
+    check_scalar(f);
+    ScalarRef r;
+    r.img.kind = f.kind;
+    r.img.n = f.n_terms;
+    r.img.constant = f.constant;
+    r.img.g0 = f.gradient[0];
+    r.img.g1 = f.gradient[1];
+    r.img.neg_sharpness = -f.sharpness;
+    const size_t n = static_cast<size_t>(f.n_terms);
+    if (f.kind == SMC_SCALAR_COSINE && n) {
+        r.amp = im.add(f.amplitude, n * sizeof(double));
+        r.freq = im.add(f.freq, 2 * n * sizeof(double));
+        r.phase = im.add(f.phase, n * sizeof(double));
+    } else if (f.kind == SMC_SCALAR_BUMPS && n) {
+        r.amp = im.add(f.amplitude, n * sizeof(double));
+        r.center = im.add(f.center, 2 * n * sizeof(double));
+    } else {
+        r.img.n = (f.kind == SMC_SCALAR_COSINE || f.kind == SMC_SCALAR_BUMPS) ? 0 : r.img.n;
+    }
+    return r;
+}
+
+ScalarImg patch(const ScalarRef& r, unsigned char* base) {
+    ScalarImg s = r.img;
+    s.amp = reinterpret_cast<const double*>(base + r.amp);
+    s.freq = reinterpret_cast<const double*>(base + r.freq);
+    s.phase = reinterpret_cast<const double*>(base + r.phase);
+    s.center = reinterpret_cast<const double*>(base + r.center);
+    return s;
+}
+
+struct VelRef {
+    VelImg img{};
+    size_t modes = 0, tile_rows = 0, tile_row = 0, coefs = 0;
+    int64_t n_coef = 0, n_row0 = 0;
+};
+
+// Velocity image: strict mode list + lattice structure + n_samples
+// coefficient sets (fills[i] for sample i).
+VelRef add_velocity(Image& im, const PreparedVelocity& v, const std::vector<const PreparedVelocity*>& fills) {
+    VelRef r;
+    r.img.is_constant = v.is_constant ? 1 : 0;
+    r.img.c1 = v.c1;
+    r.img.c2 = v.c2;
+    r.img.K = v.K;
+    r.img.n_modes = static_cast<int32_t>(v.modes.size());
+    if (v.is_constant) return r;
+    std::vector<ModeImg> modes;
+    modes.reserve(v.modes.size());
+    for (const auto& m : v.modes) {
+        const double kn = std::sqrt(double(m.k1) * m.k1 + double(m.k2) * m.k2);  // fields.cpp:66
+        modes.push_back(ModeImg{m.k1, m.k2, m.re, m.im, -double(m.k2) / kn, double(m.k1) / kn});
+    }
+    r.modes = im.add_vec(modes);
+    const LatticeHost L = lattice_structure(v);
+    r.tile_rows = im.add_vec(L.tile_rows);
+    r.tile_row = im.add_vec(L.tile_row);
+    const int64_t stride = L.stride();
+    r.coefs = im.reserve(static_cast<size_t>(stride) * fills.size() * sizeof(double));
+    for (size_t b = 0; b < fills.size(); ++b)
+        lattice_fill(L, *fills[b], reinterpret_cast<double*>(im.bytes.data() + r.coefs) + b * stride);
+    LatticeImg& li = r.img.lat;
+    li.sample_stride = stride;
+    li.K = L.K;
+    li.R = L.R;
+    li.J = L.J;
+    li.J0 = L.J0;
+    li.n_tiles = L.n_tiles;
+    r.n_coef = static_cast<int64_t>(L.coef.size());
+    r.n_row0 = static_cast<int64_t>(L.row0.size());
+    return r;
+}
+
+VelImg patch(const VelRef& r, unsigned char* base) {
+    VelImg v = r.img;
+    if (v.is_constant) return v;
+    v.modes = reinterpret_cast<const ModeImg*>(base + r.modes);
+    v.lat.tile_rows = reinterpret_cast<const int32_t*>(base + r.tile_rows);
+    v.lat.tile_row = reinterpret_cast<const int2*>(base + r.tile_row);
+    const double* c = reinterpret_cast<const double*>(base + r.coefs);
+    v.lat.coef = c;
+    v.lat.row0 = c + r.n_coef;
+    v.lat.g0 = c + r.n_coef + r.n_row0;
+    return v;
+}
+
+// Everything a K1 launch needs, prepared and uploaded.
+struct AdPrepared {
+    AdLaunch L{};
+    int64_t n_obs = 0;
+    int64_t steps_per_particle_sum = 0;  // sum_j n_j
+};
+
+void check_particle_range(int64_t n_particles) {
+    // Stream keys carry the particle index in 32 bits (rng.cpp:46-47); the
+    // reference's work lambda throws and map_reduce reports it.
+    if (n_particles > (int64_t(1) << 32)) raise(SMC_ERUNTIME, "map_reduce: a particle work function threw");
+}
+
+AdPrepared prepare_ad(smc_ctx* ctx, const smc_ad_problem& p, const std::vector<const PreparedVelocity*>& fills,
+                      const PreparedVelocity& structure, int64_t obs_begin, int64_t obs_count) {
+    const double dt = ad_resolved_dt(p);
+    const double sigma = std::sqrt(2.0 * p.kappa);
+    Image im;
+    std::vector<AdObsImg> obs;
+    AdPrepared out;
+    for (int64_t j = obs_begin; j < obs_begin + obs_count; ++j) {
+        obs.push_back(make_ad_obs(p.obs_t[j], p.obs_x[2 * j], p.obs_x[2 * j + 1], dt, sigma));
+        out.steps_per_particle_sum += obs.back().n_steps;
+    }
+    const size_t obs_off = im.add_vec(obs);
+    const ScalarRef th = add_scalar(im, p.initial_condition);
+    const VelRef vr = add_velocity(im, structure, fills);
+    unsigned char* base = ctx->upload(im);
+    AdLaunch& L = out.L;
+    L.vel = patch(vr, base);
+    L.theta0 = patch(th, base);
+    L.obs = reinterpret_cast<const AdObsImg*>(base + obs_off);
+    L.n_obs = static_cast<int32_t>(obs_count);
+    L.obs_slot0 = static_cast<uint32_t>(obs_begin);
+    L.n_particles = p.n_particles;
+    L.p_begin = 0;
+    L.p_end = p.n_particles;
+    L.n_samples = 1;
+    L.precision = p.precision;
+    L.sigma = sigma;
+    out.n_obs = obs_count;
+    return out;
+}
+
+void run_particles(smc_ctx* ctx, AdLaunch& L) {
+    if (L.precision == SMC_FP64_STRICT) {
+        if (L.n_samples != 1) raise(SMC_EINVAL, "strict precision is single-sample only");
+        if (!L.vel.is_constant && L.vel.K > 128) raise(SMC_EINVAL, "strict precision supports max_wavenumber <= 128");
+        CK(launch_ad_particles_strict(L, ctx->stream));
+    } else if (L.precision == SMC_FP32) {
+        CK(launch_ad_particles_fp32(L, ctx->stream));
+    } else {
+        CK(launch_ad_particles(L, ctx->stream));
+    }
+    count_launches(ctx, 1);
+}
+
+// Reduce [n_seg][n] values (no failures) into estimates on the host.
+void reduce_ad(smc_ctx* ctx, const double* values, int64_t n, int64_t n_seg, smc_estimate* out) {
+    cudaStream_t s = ctx->stream;
+    const int64_t chunks = (n + kChunk - 1) / kChunk;
+    double* scratch = ctx->scratch.get<double>(static_cast<size_t>(2 * n_seg * std::max<int64_t>(chunks, 1)));
+    double* sums = ctx->sums.get<double>(static_cast<size_t>(n_seg));
+    double* means = ctx->means.get<double>(static_cast<size_t>(n_seg));
+    double* sumsq = ctx->sumsq.get<double>(static_cast<size_t>(n_seg));
+    smc_estimate* est = ctx->est.get<smc_estimate>(static_cast<size_t>(n_seg));
+    int launches = 0;
+    CK(tree_reduce(values, n, nullptr, n, n_seg, sums, nullptr, 0, scratch, s, &launches));
+    CK(launch_divide(sums, nullptr, n, n_seg, means, s));
+    CK(tree_reduce(values, n, nullptr, n, n_seg, sumsq, means, 1, scratch, s, &launches));
+    CK(launch_estimates(means, sumsq, nullptr, nullptr, n, n, n_seg, est, s));
+    count_launches(ctx, launches + 2);
+    smc_estimate* h = ctx->est_host.get<smc_estimate>(static_cast<size_t>(n_seg));
+    CK(cudaMemcpyAsync(h, est, sizeof(smc_estimate) * n_seg, cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(ctx->ev[2], s));
+    CK(cudaStreamSynchronize(s));
+    std::memcpy(out, h, sizeof(smc_estimate) * n_seg);
+}
+
+void finish_stats(smc_ctx* ctx) {
+    float a = 0.f, b = 0.f;
+    CK(cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]));
+    CK(cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]));
+    ctx->stats.particle_kernel_ms = a;
+    ctx->stats.reduce_ms = b;
+}
+
+void ad_observe_range(smc_ctx* ctx, const smc_ad_problem& p, uint64_t seed, int64_t obs_begin, int64_t obs_count,
+                      smc_estimate* out) {
+    const PreparedVelocity v = prepare_velocity(p.velocity);
+    check_kappa(p.kappa);
+    check_scalar(p.initial_condition);
+    ad_validate(p);
+    check_particle_range(p.n_particles);
+    ctx->stats = smc_stats{};
+    AdPrepared P = prepare_ad(ctx, p, {&v}, v, obs_begin, obs_count);
+    P.L.seed = seed;
+    const int64_t n = p.n_particles;
+    P.L.values = ctx->values.get<double>(static_cast<size_t>(obs_count * n));
+    CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+    run_particles(ctx, P.L);
+    CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+    reduce_ad(ctx, P.L.values, n, obs_count, out);
+    finish_stats(ctx);
+    ctx->stats.particle_steps = P.steps_per_particle_sum * n;
+}
+
+BvpLaunch prepare_bvp(smc_ctx* ctx, const smc_bvp_problem& p, int64_t obs_begin, int64_t obs_count) {
+    const PreparedVelocity v = prepare_velocity(p.velocity);
+    check_kappa(p.kappa);
+    check_scalar(p.forcing);
+    check_scalar(p.boundary_data);
+    check_domain(p.domain);
+    bvp_validate(p);
+    check_particle_range(p.n_particles);
+    const double dt = bvp_resolved_dt(p, v);
+    Image im;
+    const size_t obs_off = im.add(p.obs_x + 2 * obs_begin, static_cast<size_t>(2 * obs_count) * sizeof(double));
+    const ScalarRef fr = add_scalar(im, p.forcing);
+    const ScalarRef br = add_scalar(im, p.boundary_data);
+    const VelRef vr = add_velocity(im, v, {&v});
+    unsigned char* base = ctx->upload(im);
+    BvpLaunch L{};
+    L.vel = patch(vr, base);
+    L.forcing = patch(fr, base);
+    L.boundary = patch(br, base);
+    DomainImg& d = L.domain;
+    d.kind = p.domain.kind;
+    d.lo1 = p.domain.lower[0];
+    d.lo2 = p.domain.lower[1];
+    d.hi1 = p.domain.upper[0];
+    d.hi2 = p.domain.upper[1];
+    d.c1 = p.domain.center[0];
+    d.c2 = p.domain.center[1];
+    d.r = p.domain.radius;
+    d.r2 = p.domain.radius * p.domain.radius;
+    L.obs_x = reinterpret_cast<const double*>(base + obs_off);
+    L.n_obs = static_cast<int32_t>(obs_count);
+    L.obs_slot0 = static_cast<uint32_t>(obs_begin);
+    L.n_particles = p.n_particles;
+    L.max_steps = p.max_steps;
+    L.dt = dt;
+    L.sigma = std::sqrt(2.0 * p.kappa);
+    L.root_dt = std::sqrt(dt);
+    L.sr = L.sigma * L.root_dt;
+    L.precision = p.precision;
+    return L;
+}
+
+void run_bvp(smc_ctx* ctx, BvpLaunch& L, int64_t n_obs, int64_t n) {
+    cudaStream_t s = ctx->stream;
+    const size_t total = static_cast<size_t>(n_obs * n);
+    L.values = ctx->values.get<double>(total);
+    L.aux = ctx->aux.get<double>(total);
+    L.failed = ctx->flags.get<uint8_t>(total);
+    // walker-queue head + step total; ctx->counts is reused for the valid
+    // counts only after the kernel has finished with these.
+    unsigned long long* ctr = ctx->flags2.get<unsigned long long>(2);
+    CK(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), s));
+    L.counter = ctr;
+    L.step_total = ctr + 1;
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    CK(cudaEventRecord(ctx->ev[0], s));
+    if (L.precision == SMC_FP64_STRICT) {
+        if (!L.vel.is_constant && L.vel.K > 128) raise(SMC_EINVAL, "strict precision supports max_wavenumber <= 128");
+        CK(launch_bvp_walkers_strict(L, sms, s));
+    } else {
+        CK(launch_bvp_walkers(L, sms, s));
+    }
+    count_launches(ctx, 1);
+    CK(cudaEventRecord(ctx->ev[1], s));
+}
+
+}  // namespace
+
+extern "C" {
+
+int smc_abi_version(void) { return SMC_ABI_VERSION; }
+
+const char* smc_last_error(void) { return g_err.c_str(); }
+
+smc_status smc_create(int device, smc_ctx** out) {
+    return guarded([&] {
+        *out = nullptr;
+        int n = 0;
+        CK(cudaGetDeviceCount(&n));
+        if (device < 0 || device >= n) raise(SMC_ECUDA, "smc_create: no such CUDA device");
+        CK(cudaSetDevice(device));
+        auto* c = new smc_ctx();
+        c->device = device;
+        CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+        c->stream = c->own_stream;
+        for (auto& e : c->ev) CK(cudaEventCreate(&e));
+        *out = c;
+    });
+}
+
+void smc_destroy(smc_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->own_stream) cudaStreamSynchronize(ctx->own_stream);
+    for (DevBuf* b : {&ctx->image, &ctx->values, &ctx->aux, &ctx->flags, &ctx->flags2, &ctx->scratch, &ctx->sums, &ctx->means,
+                      &ctx->sumsq, &ctx->sumaux, &ctx->est, &ctx->counts, &ctx->tmp_a, &ctx->tmp_b, &ctx->tmp_c})
+        b->release();
+    ctx->staging.release();
+    ctx->est_host.release();
+    for (auto& e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+}
+
+void* smc_stream(smc_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+smc_status smc_set_stream(smc_ctx* ctx, void* stream) {
+    return guarded([&] {
+        CK(cudaSetDevice(ctx->device));
+        CK(cudaStreamSynchronize(ctx->stream));
+        ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    });
+}
+
+smc_status smc_ad_resolved_dt(const smc_ad_problem* p, double* out) {
+    return guarded([&] { *out = ad_resolved_dt(*p); });
+}
+
+smc_status smc_bvp_resolved_dt(const smc_bvp_problem* p, double* out) {
+    return guarded([&] {
+        const PreparedVelocity v = prepare_velocity(p->velocity);
+        *out = bvp_resolved_dt(*p, v);
+    });
+}
+
+smc_status smc_velocity_validate(const smc_velocity* v) {
+    return guarded([&] { (void)prepare_velocity(*v); });
+}
+
+smc_status smc_ad_validate(const smc_ad_problem* p) {
+    return guarded([&] {
+        (void)prepare_velocity(p->velocity);
+        check_kappa(p->kappa);
+        check_scalar(p->initial_condition);
+        ad_validate(*p);
+    });
+}
+
+smc_status smc_bvp_validate(const smc_bvp_problem* p) {
+    return guarded([&] {
+        (void)prepare_velocity(p->velocity);
+        check_kappa(p->kappa);
+        check_scalar(p->forcing);
+        check_scalar(p->boundary_data);
+        check_domain(p->domain);
+        bvp_validate(*p);
+    });
+}
+
+int smc_struct_sizes(int64_t* out, int cap) {
+    const int64_t s[] = {sizeof(smc_estimate), sizeof(smc_scalar_field), sizeof(smc_velocity),
+                         sizeof(smc_ad_problem), sizeof(smc_domain), sizeof(smc_bvp_problem),
+                         sizeof(smc_prior), sizeof(smc_stats)};
+    const int n = static_cast<int>(sizeof(s) / sizeof(s[0]));
+    for (int i = 0; i < n && i < cap; ++i) out[i] = s[i];
+    return n;
+}
+
+int64_t smc_num_chunks(int64_t n_particles) { return (n_particles + kChunk - 1) / kChunk; }
+
+smc_status smc_ad_observe(smc_ctx* ctx, const smc_ad_problem* p, uint64_t seed, smc_estimate* out) {
+    return guarded([&] {
+        CK(cudaSetDevice(ctx->device));
+        ad_observe_range(ctx, *p, seed, 0, p->n_obs, out);
+    });
+}
+
+smc_status smc_ad_observe_single(smc_ctx* ctx, const smc_ad_problem* p, uint64_t obs_index, uint64_t seed,
+                                 smc_estimate* out) {
+    return guarded([&] {
+        CK(cudaSetDevice(ctx->device));
+        // observe_ad_single validates first, then range-checks (forward_ad.cpp:64-67).
+        (void)prepare_velocity(p->velocity);
+        check_kappa(p->kappa);
+        check_scalar(p->initial_condition);
+        ad_validate(*p);
+        if (obs_index >= static_cast<uint64_t>(p->n_obs))
+            raise(SMC_ERANGE, "observe_ad_single: observation index out of range");
+        ad_observe_range(ctx, *p, seed, static_cast<int64_t>(obs_index), 1, out);
+    });
+}
+
+smc_status smc_ad_observe_batched(smc_ctx* ctx, const smc_ad_problem* base, const smc_prior* prior,
+                                  int64_t n_samples, const double* u, const uint64_t* seeds, uint64_t seed,
+                                  smc_estimate* out) {
+    return guarded([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (n_samples < 1) raise(SMC_EINVAL, "observe_ad_batched: need at least one sample");
+        if (prior->cutoff <= 0) raise(SMC_EINVAL, "FourierVelocityField: max_wavenumber must be positive");
+        const std::vector<HostMode> pm = prior_modes(prior->cutoff);
+        const int64_t dim = 2 * static_cast<int64_t>(pm.size());
+        // One FourierVelocityField per sample, from u in prior order
+        // (velocity_from_coefficients, inference.cpp:63-73).
+        std::vector<PreparedVelocity> fields(static_cast<size_t>(n_samples));
+        std::vector<const PreparedVelocity*> fills;
+        fills.reserve(static_cast<size_t>(n_samples));
+        for (int64_t b = 0; b < n_samples; ++b) {
+            smc_velocity sv{};
+            std::vector<int32_t> k(static_cast<size_t>(dim));
+            for (size_t i = 0; i < pm.size(); ++i) {
+                k[2 * i] = pm[i].k1;
+                k[2 * i + 1] = pm[i].k2;
+            }
+            sv.is_constant = 0;
+            sv.max_wavenumber = prior->cutoff;
+            sv.n_modes = static_cast<int64_t>(pm.size());
+            sv.k = k.data();
+            sv.coeff = u + b * dim;
+            fields[static_cast<size_t>(b)] = prepare_velocity(sv);
+            fills.push_back(&fields[static_cast<size_t>(b)]);
+        }
+        smc_ad_problem p = *base;
+        p.velocity.is_constant = 0;
+        p.velocity.max_wavenumber = prior->cutoff;
+        check_kappa(p.kappa);
+        check_scalar(p.initial_condition);
+        // validate() without the velocity slot
+        ad_validate(p);
+        check_particle_range(p.n_particles);
+        if (p.precision == SMC_FP64_STRICT) raise(SMC_EINVAL, "strict precision is single-sample only");
+        ctx->stats = smc_stats{};
+        const int64_t n = p.n_particles, n_obs = p.n_obs;
+        AdPrepared P = prepare_ad(ctx, p, fills, fields[0], 0, n_obs);
+        uint64_t* d_seeds = nullptr;
+        if (seeds) {
+            d_seeds = ctx->tmp_a.get<uint64_t>(static_cast<size_t>(n_samples));
+            CK(cudaMemcpyAsync(d_seeds, seeds, sizeof(uint64_t) * n_samples, cudaMemcpyHostToDevice, ctx->stream));
+        }
+        double* values = ctx->values.get<double>(static_cast<size_t>(n_samples * n_obs * n));
+        CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+        constexpr int64_t kMaxZ = 65535;
+        for (int64_t b0 = 0; b0 < n_samples; b0 += kMaxZ) {
+            const int64_t nb = std::min(kMaxZ, n_samples - b0);
+            AdLaunch L = P.L;
+            L.seed = seed;
+            L.seeds = d_seeds ? d_seeds + b0 : nullptr;
+            L.n_samples = static_cast<int32_t>(nb);
+            if (!L.vel.is_constant) {
+                const int64_t off = b0 * L.vel.lat.sample_stride;
+                L.vel.lat.coef += off;
+                L.vel.lat.row0 += off;
+                L.vel.lat.g0 += off;
+            }
+            L.values = values + b0 * n_obs * n;
+            run_particles(ctx, L);
+        }
+        CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+        reduce_ad(ctx, values, n, n_samples * n_obs, out);
+        finish_stats(ctx);
+        ctx->stats.particle_steps = P.steps_per_particle_sum * n * n_samples;
+    });
+}
+
+smc_status smc_ad_shard_partials(smc_ctx* ctx, const smc_ad_problem* p, uint64_t seed, int64_t chunk_begin,
+                                 int64_t chunk_end, double* partials_dev) {
+    return guarded([&] {
+        CK(cudaSetDevice(ctx->device));
+        const PreparedVelocity v = prepare_velocity(p->velocity);
+        check_kappa(p->kappa);
+        check_scalar(p->initial_condition);
+        ad_validate(*p);
+        check_particle_range(p->n_particles);
+        const int64_t n_chunks = smc_num_chunks(p->n_particles);
+        if (chunk_begin < 0 || chunk_end > n_chunks || chunk_begin > chunk_end)
+            raise(SMC_ERANGE, "smc_ad_shard_partials: chunk range out of bounds");
+        ctx->stats = smc_stats{};
+        AdPrepared P = prepare_ad(ctx, *p, {&v}, v, 0, p->n_obs);
+        P.L.seed = seed;
+        P.L.p_begin = chunk_begin * kChunk;
+        P.L.p_end = std::min(chunk_end * kChunk, p->n_particles);
+        const int64_t span = std::max<int64_t>(P.L.p_end - P.L.p_begin, 0);
+        P.L.values = ctx->values.get<double>(static_cast<size_t>(std::max<int64_t>(p->n_obs * span, 1)));
+        CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+        run_particles(ctx, P.L);
+        CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+        const int64_t nloc = chunk_end - chunk_begin;
+        if (nloc > 0) {
+            CK(launch_tree_pass(P.L.values, span, nullptr, span, p->n_obs, partials_dev, nloc, nullptr, 0, ctx->stream));
+            count_launches(ctx, 1);
+        }
+        CK(cudaEventRecord(ctx->ev[2], ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        finish_stats(ctx);
+        ctx->shard_n_obs = p->n_obs;
+        ctx->shard_span = span;
+        ctx->stats.particle_steps = P.steps_per_particle_sum * span;
+    });
+}
+
+smc_status smc_tree_finish(smc_ctx* ctx, const double* partials_dev, int64_t n_obs, int64_t n_chunks,
+                           double* sums_dev) {
+    return guarded([&] {
+        CK(cudaSetDevice(ctx->device));
+        double* scratch = ctx->scratch.get<double>(static_cast<size_t>(2 * n_obs * std::max<int64_t>(1, n_chunks)));
+        int launches = 0;
+        CK(tree_reduce(partials_dev, n_chunks, nullptr, n_chunks, n_obs, sums_dev, nullptr, 0, scratch, ctx->stream,
+                       &launches));
+        count_launches(ctx, launches);
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+smc_status smc_ad_shard_sq_partials(smc_ctx* ctx, const double* means_dev, int64_t n_obs, int64_t chunk_begin,
+                                    int64_t chunk_end, double* partials_dev) {
+    return guarded([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (n_obs != ctx->shard_n_obs) raise(SMC_EINVAL, "smc_ad_shard_sq_partials: observation count mismatch");
+        const int64_t nloc = chunk_end - chunk_begin;
+        const int64_t span = ctx->shard_span;
+        if (nloc > 0) {
+            CK(launch_tree_pass(static_cast<const double*>(ctx->values.p), span, nullptr, span, n_obs, partials_dev,
+                                nloc, means_dev, 1, ctx->stream));
+            count_launches(ctx, 1);
+        }
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+smc_status smc_ad_particle_values(smc_ctx* ctx, const smc_ad_problem* p, uint64_t obs_index, uint64_t seed,
+                                  int64_t n, double* out) {
+    return guarded([&] {
+        CK(cudaSetDevice(ctx->device));
+        const PreparedVelocity v = prepare_velocity(p->velocity);
+        check_kappa(p->kappa);
+        check_scalar(p->initial_condition);
+        ad_validate(*p);
+        if (obs_index >= static_cast<uint64_t>(p->n_obs)) raise(SMC_ERANGE, "observation index out of range");
+        AdPrepared P = prepare_ad(ctx, *p, {&v}, v, static_cast<int64_t>(obs_index), 1);
+        P.L.seed = seed;
+        P.L.p_end = n;
+        P.L.values = ctx->values.get<double>(static_cast<size_t>(n));
+        run_particles(ctx, P.L);
+        CK(cudaMemcpyAsync(out, P.L.values, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+smc_status smc_philox_device(smc_ctx* ctx, int64_t n, const uint32_t* ctr, const uint32_t* key, uint32_t* out) {
+    return guarded([&] {
+        CK(cudaSetDevice(ctx->device));
+        uint32_t* dc = ctx->tmp_a.get<uint32_t>(static_cast<size_t>(4 * n));
+        uint32_t* dk = ctx->tmp_b.get<uint32_t>(static_cast<size_t>(2 * n));
+        uint32_t* dout = ctx->tmp_c.get<uint32_t>(static_cast<size_t>(4 * n));
+        CK(cudaMemcpyAsync(dc, ctr, 16 * n, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(dk, key, 8 * n, cudaMemcpyHostToDevice, ctx->stream));
+        CK(launch_philox(n, dc, dk, dout, ctx->stream));
+        CK(cudaMemcpyAsync(out, dout, 16 * n, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+smc_status smc_normal_pairs_device(smc_ctx* ctx, uint64_t seed, uint64_t obs, uint64_t particle, int64_t n_blocks,
+                                   double* out) {
+    return guarded([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (obs > 0xFFFFFFFFull || particle > 0xFFFFFFFFull)
+            raise(SMC_EINVAL, "StreamKey: obs/particle index exceeds 32-bit stream space");
+        double* d = ctx->tmp_a.get<double>(static_cast<size_t>(2 * n_blocks));
+        CK(launch_normal_pairs(seed, static_cast<uint32_t>(obs), static_cast<uint32_t>(particle), n_blocks, d,
+                               ctx->stream));
+        CK(cudaMemcpyAsync(out, d, 16 * n_blocks, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+smc_status smc_last_stats(smc_ctx* ctx, smc_stats* out) {
+    return guarded([&] {
+        *out = ctx->stats;
+        out->total_launches = ctx->total_launches;
+    });
+}
+
+smc_status smc_fp64_peak(smc_ctx* ctx, double ms, double* tflops) {
+    return guarded([&] {
+        CK(cudaSetDevice(ctx->device));
+        int sms = 0;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+        const int blocks = sms * 8;
+        double* sink = ctx->tmp_a.get<double>(static_cast<size_t>(blocks));
+        int iters = 4096;
+        float t = 0.f;
+        for (int attempt = 0; attempt < 8; ++attempt) {
+            CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+            CK(launch_dfma_peak(blocks, iters, sink, ctx->stream));
+            CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+            CK(cudaEventSynchronize(ctx->ev[1]));
+            CK(cudaEventElapsedTime(&t, ctx->ev[0], ctx->ev[1]));
+            if (t >= 0.9 * ms) break;
+            const double scale = std::min(64.0, std::max(2.0, ms / std::max<double>(t, 1e-3)));
+            iters = static_cast<int>(std::min<double>(iters * scale, 1 << 30));
+        }
+        const double flops = 2.0 * 8.0 * double(iters) * 256.0 * blocks;
+        *tflops = flops / (double(t) * 1e-3) / 1e12;
+    });
+}
+
+smc_status smc_bvp_observe(smc_ctx* ctx, const smc_bvp_problem* p, uint64_t seed, smc_estimate* out) {
+    return guarded([&] {
+        CK(cudaSetDevice(ctx->device));
+        ctx->stats = smc_stats{};
+        BvpLaunch L = prepare_bvp(ctx, *p, 0, p->n_obs);
+        L.seed = seed;
+        const int64_t n = p->n_particles, n_obs = p->n_obs;
+        run_bvp(ctx, L, n_obs, n);
+        // compaction of valid walkers, then the same tree as AD
+        cudaStream_t s = ctx->stream;
+        const int64_t chunks = smc_num_chunks(n);
+        double* cvalues = ctx->tmp_a.get<double>(static_cast<size_t>(n_obs * n));
+        double* caux = ctx->tmp_b.get<double>(static_cast<size_t>(n_obs * n));
+        int64_t* chunk_tmp = ctx->tmp_c.get<int64_t>(static_cast<size_t>(2 * n_obs * chunks));
+        int64_t* counts = ctx->counts.get<int64_t>(static_cast<size_t>(n_obs));
+        CK(compact_valid(L.values, L.aux, L.failed, n, n_obs, cvalues, caux, counts, chunk_tmp, s));
+        double* scratch = ctx->scratch.get<double>(static_cast<size_t>(2 * n_obs * std::max<int64_t>(chunks, 1)));
+        double* sums = ctx->sums.get<double>(static_cast<size_t>(n_obs));
+        double* means = ctx->means.get<double>(static_cast<size_t>(n_obs));
+        double* sumsq = ctx->sumsq.get<double>(static_cast<size_t>(n_obs));
+        double* sumaux = ctx->sumaux.get<double>(static_cast<size_t>(n_obs));
+        smc_estimate* est = ctx->est.get<smc_estimate>(static_cast<size_t>(n_obs));
+        int launches = 3;
+        CK(tree_reduce(cvalues, n, counts, n, n_obs, sums, nullptr, 0, scratch, s, &launches));
+        CK(launch_divide(sums, counts, n, n_obs, means, s));
+        CK(tree_reduce(cvalues, n, counts, n, n_obs, sumsq, means, 1, scratch, s, &launches));
+        CK(tree_reduce(caux, n, counts, n, n_obs, sumaux, nullptr, 0, scratch, s, &launches));
+        CK(launch_estimates(means, sumsq, sumaux, counts, n, n, n_obs, est, s));
+        count_launches(ctx, launches + 2);
+        smc_estimate* h = ctx->est_host.get<smc_estimate>(static_cast<size_t>(n_obs));
+        CK(cudaMemcpyAsync(h, est, sizeof(smc_estimate) * n_obs, cudaMemcpyDeviceToHost, s));
+        unsigned long long* steps_h = ctx->staging.get<unsigned long long>(1);
+        CK(cudaMemcpyAsync(steps_h, L.step_total, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(ctx->ev[2], s));
+        CK(cudaStreamSynchronize(s));
+        ctx->stats.particle_steps = static_cast<int64_t>(*steps_h);
+        finish_stats(ctx);
+        for (int64_t j = 0; j < n_obs; ++j)
+            if (h[j].n_failed == n) raise(SMC_ERUNTIME, "map_reduce: every particle of an observation failed");
+        std::memcpy(out, h, sizeof(smc_estimate) * n_obs);
+    });
+}
+
+smc_status smc_bvp_particle_values(smc_ctx* ctx, const smc_bvp_problem* p, uint64_t obs_index, uint64_t seed,
+                                   int64_t n, double* values, double* aux, uint8_t* failed) {
+    return guarded([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (obs_index >= static_cast<uint64_t>(p->n_obs)) raise(SMC_ERANGE, "observation index out of range");
+        BvpLaunch L = prepare_bvp(ctx, *p, static_cast<int64_t>(obs_index), 1);
+        L.seed = seed;
+        L.n_particles = n;
+        run_bvp(ctx, L, 1, n);
+        CK(cudaMemcpyAsync(values, L.values, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(aux, L.aux, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(failed, L.failed, n, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+}  // extern "C"

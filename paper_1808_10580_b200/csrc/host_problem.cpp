@@ -1,0 +1,282 @@
+// host_problem.cpp — validation, canonicalisation and packing on the host.
+// Messages and exception classes follow the reference exactly so the C++ shim
+// (host/scalarmc_forward_gpu.cpp) can rethrow the same std:: types.
+#include "host_problem.h"
+
+#include <algorithm>
+#include <cmath>
+#include <limits>
+
+namespace smc {
+
+void raise(int code, const std::string& msg) { throw Error{code, msg}; }
+
+namespace {
+bool is_canonical(int k1, int k2) { return k1 > 0 || (k1 == 0 && k2 > 0); }  // fields.cpp:15
+}  // namespace
+
+PreparedVelocity prepare_velocity(const smc_velocity& v) {
+    PreparedVelocity out;
+    if (v.is_constant) {
+        out.is_constant = true;
+        out.c1 = v.constant[0];
+        out.c2 = v.constant[1];
+        return out;
+    }
+    out.is_constant = false;
+    if (v.max_wavenumber <= 0) raise(SMC_EINVAL, "FourierVelocityField: max_wavenumber must be positive");
+    out.K = v.max_wavenumber;
+    if (v.n_modes < 0) raise(SMC_EINVAL, "FourierVelocityField: negative mode count");
+    out.modes.reserve(static_cast<size_t>(v.n_modes));
+    for (int64_t i = 0; i < v.n_modes; ++i) {
+        HostMode m{v.k[2 * i], v.k[2 * i + 1], v.coeff[2 * i], v.coeff[2 * i + 1]};
+        if (m.k1 == 0 && m.k2 == 0) raise(SMC_EINVAL, "FourierVelocityField: k = (0,0) is not allowed");
+        const double kn2 = double(m.k1) * m.k1 + double(m.k2) * m.k2;
+        if (kn2 > double(out.K) * out.K + 1e-9) raise(SMC_EINVAL, "FourierVelocityField: |k| exceeds max_wavenumber");
+        if (!std::isfinite(m.re) || !std::isfinite(m.im))
+            raise(SMC_EINVAL, "FourierVelocityField: non-finite coefficient");
+        if (!is_canonical(m.k1, m.k2)) m = HostMode{-m.k1, -m.k2, -m.re, m.im};  // v_k = -conj(v_-k)
+        out.modes.push_back(m);
+    }
+    std::sort(out.modes.begin(), out.modes.end(), [](const HostMode& a, const HostMode& b) {
+        return a.k1 != b.k1 ? a.k1 < b.k1 : a.k2 < b.k2;
+    });
+    for (size_t i = 1; i < out.modes.size(); ++i)
+        if (out.modes[i].k1 == out.modes[i - 1].k1 && out.modes[i].k2 == out.modes[i - 1].k2)
+            raise(SMC_EINVAL, "FourierVelocityField: duplicate mode (both members of a +/-k pair given?)");
+    return out;
+}
+
+double amplitude_bound(const PreparedVelocity& v) {
+    if (v.is_constant) return std::hypot(v.c1, v.c2);
+    double s = 0.0;
+    for (const auto& m : v.modes) s += 2.0 * std::hypot(m.re, m.im);
+    return s;
+}
+
+void check_kappa(double kappa) {
+    if (!(kappa >= 0.0)) raise(SMC_EINVAL, "DiffusionModel: kappa must be >= 0");
+}
+
+void check_scalar(const smc_scalar_field& f) {
+    if (f.kind < SMC_SCALAR_CONSTANT || f.kind > SMC_SCALAR_LINEAR) raise(SMC_EINVAL, "ScalarField: unknown kind");
+    if (f.n_terms < 0) raise(SMC_EINVAL, "ScalarField: negative term count");
+    if (f.kind == SMC_SCALAR_BUMPS && !(f.sharpness > 0.0))
+        raise(SMC_EINVAL, "ScalarField: sharpness must be positive");
+    if (f.kind == SMC_SCALAR_COSINE && f.n_terms > 0 && (!f.amplitude || !f.freq || !f.phase))
+        raise(SMC_EINVAL, "ScalarField: cosine terms need amplitude, freq and phase arrays");
+    if (f.kind == SMC_SCALAR_BUMPS && f.n_terms > 0 && (!f.amplitude || !f.center))
+        raise(SMC_EINVAL, "ScalarField: bumps need amplitude and center arrays");
+}
+
+void check_domain(const smc_domain& d) {
+    if (d.kind == SMC_DOMAIN_BOX && !(d.lower[0] < d.upper[0] && d.lower[1] < d.upper[1]))
+        raise(SMC_EINVAL, "Domain::box: lower corner must be strictly below upper");
+    if (d.kind == SMC_DOMAIN_DISK && !(d.radius > 0.0)) raise(SMC_EINVAL, "Domain::disk: radius must be positive");
+    if (d.kind < SMC_DOMAIN_TORUS || d.kind > SMC_DOMAIN_DISK) raise(SMC_EINVAL, "Domain: unknown kind");
+}
+
+double ad_resolved_dt(const smc_ad_problem& p) {
+    if (p.dt > 0.0) return p.dt;
+    double t_min = std::numeric_limits<double>::infinity();
+    for (int64_t j = 0; j < p.n_obs; ++j) t_min = std::min(t_min, p.obs_t[j]);
+    return t_min / 200.0;
+}
+
+void ad_validate(const smc_ad_problem& p) {
+    if (p.n_obs <= 0) raise(SMC_EINVAL, "AdProblemSpec: no observations");
+    for (int64_t j = 0; j < p.n_obs; ++j) {
+        const double t = p.obs_t[j], x1 = p.obs_x[2 * j], x2 = p.obs_x[2 * j + 1];
+        if (!(t > 0.0)) raise(SMC_EINVAL, "AdProblemSpec: observation times must be positive");
+        if (!std::isfinite(x1) || !std::isfinite(x2)) raise(SMC_EINVAL, "AdProblemSpec: non-finite observation point");
+        if (x1 < 0.0 || x1 >= 1.0 || x2 < 0.0 || x2 >= 1.0)
+            raise(SMC_EINVAL, "AdProblemSpec: observation points must lie in [0,1)^2");
+    }
+    if (p.n_particles < 2) raise(SMC_EINVAL, "AdProblemSpec: need at least two particles");
+    if (p.scheme != SMC_EULER_MARUYAMA && p.scheme != SMC_MILSTEIN) raise(SMC_EINVAL, "AdProblemSpec: unknown scheme");
+    if (p.precision < SMC_FP64 || p.precision > SMC_FP64_STRICT) raise(SMC_EINVAL, "AdProblemSpec: unknown precision");
+}
+
+bool domain_contains(const smc_domain& d, double x1, double x2) {
+    if (d.kind == SMC_DOMAIN_BOX) return x1 > d.lower[0] && x1 < d.upper[0] && x2 > d.lower[1] && x2 < d.upper[1];
+    if (d.kind == SMC_DOMAIN_DISK) {
+        const double q1 = x1 - d.center[0], q2 = x2 - d.center[1];
+        return q1 * q1 + q2 * q2 < d.radius * d.radius;
+    }
+    return true;
+}
+
+double bvp_resolved_dt(const smc_bvp_problem& p, const PreparedVelocity& v) {
+    if (p.dt > 0.0) return p.dt;
+    double diam;
+    if (p.domain.kind == SMC_DOMAIN_BOX) diam = std::hypot(p.domain.upper[0] - p.domain.lower[0], p.domain.upper[1] - p.domain.lower[1]);
+    else if (p.domain.kind == SMC_DOMAIN_DISK) diam = 2.0 * p.domain.radius;
+    else diam = 1.4142135623730951;
+    const double speed = amplitude_bound(v);
+    const double denom = 2.0 * p.kappa + speed * diam;
+    const double raw = denom > 0.0 ? 1e-3 * diam * diam / denom : 1e-2;
+    return std::clamp(raw, 1e-6, 1e-2);
+}
+
+void bvp_validate(const smc_bvp_problem& p) {
+    if (p.domain.kind == SMC_DOMAIN_TORUS) raise(SMC_EINVAL, "BvpProblemSpec: domain must be bounded");
+    if (p.n_obs <= 0) raise(SMC_EINVAL, "BvpProblemSpec: no observations");
+    for (int64_t j = 0; j < p.n_obs; ++j) {
+        const double x1 = p.obs_x[2 * j], x2 = p.obs_x[2 * j + 1];
+        if (!std::isfinite(x1) || !std::isfinite(x2)) raise(SMC_EINVAL, "BvpProblemSpec: non-finite observation point");
+        if (!domain_contains(p.domain, x1, x2))
+            raise(SMC_EINVAL, "BvpProblemSpec: observation points must be strictly interior");
+    }
+    if (p.n_particles < 2) raise(SMC_EINVAL, "BvpProblemSpec: need at least two particles");
+    if (p.max_steps < 1) raise(SMC_EINVAL, "BvpProblemSpec: max_steps must be positive");
+    if (p.scheme != SMC_EULER_MARUYAMA && p.scheme != SMC_MILSTEIN) raise(SMC_EINVAL, "BvpProblemSpec: unknown scheme");
+    if (p.precision < SMC_FP64 || p.precision > SMC_FP64_STRICT) raise(SMC_EINVAL, "BvpProblemSpec: unknown precision");
+}
+
+// ---------------------------------------------------------------------------
+// Lattice packing.  For mode (k1,k2) with coefficient c, g = 2 c / |k|; the
+// velocity is v1 = sum -k2 Re(g E), v2 = sum k1 Re(g E), E = P1[k1] P2[k2].
+// A +/-j pair of row k1 with P2[j] = r + i s contributes, with
+// alpha = g+ + g-, beta = g+ - g-:
+//   A' += k1 (alpha r + i beta s)        (v2 = Re(P1 A'))
+//   B  += -j (beta r + i alpha s)        (v1 = Re(P1 B))
+// ---------------------------------------------------------------------------
+namespace {
+
+struct Slot {
+    double gr = 0.0, gi = 0.0;
+};
+
+struct Grid {
+    int K, R = 0, J = 0, J0 = 0;
+    std::vector<Slot> g;  // [(K+1)][(2K+1)], index k1*(2K+1) + (k2+K)
+    std::vector<int> jrow;
+    explicit Grid(int K_) : K(K_), g(static_cast<size_t>(K_ + 1) * (2 * K_ + 1)), jrow(static_cast<size_t>(K_ + 1), 0) {}
+    Slot& at(int k1, int k2) { return g[static_cast<size_t>(k1) * (2 * K + 1) + (k2 + K)]; }
+};
+
+Grid make_grid(const PreparedVelocity& v, bool with_values) {
+    Grid gr(v.K);
+    for (const auto& m : v.modes) {
+        if (with_values) {
+            const double kn = std::sqrt(double(m.k1) * m.k1 + double(m.k2) * m.k2);
+            gr.at(m.k1, m.k2) = Slot{2.0 * m.re / kn, 2.0 * m.im / kn};
+        }
+        const int j = m.k2 >= 0 ? m.k2 : -m.k2;
+        if (m.k1 == 0) gr.J0 = std::max(gr.J0, j);
+        else {
+            gr.R = std::max(gr.R, m.k1);
+            gr.jrow[static_cast<size_t>(m.k1)] = std::max(gr.jrow[static_cast<size_t>(m.k1)], j);
+            gr.J = std::max(gr.J, j);
+        }
+    }
+    return gr;
+}
+
+constexpr int kTileW = 8;
+
+}  // namespace
+
+LatticeHost lattice_structure(const PreparedVelocity& v) {
+    LatticeHost L;
+    const Grid gr = make_grid(v, false);
+    L.K = v.K;
+    L.R = gr.R;
+    L.J = gr.J;
+    L.J0 = gr.J0;
+    const int jmax = std::max(gr.J, gr.J0);
+    L.n_tiles = std::max(1, (jmax + kTileW - 1) / kTileW);
+    L.tile_rows.assign(static_cast<size_t>(L.n_tiles), 0);
+    L.tile_row.assign(static_cast<size_t>(L.n_tiles) * (L.R + 1), int2{0, 0});
+    int32_t off = 0;
+    for (int t = 0; t < L.n_tiles; ++t) {
+        int last = (t == 0) ? L.R : 0;  // tile 0 folds every row's k2 = 0 term
+        for (int k1 = 1; k1 <= L.R; ++k1) {
+            const int cnt = std::clamp(gr.jrow[static_cast<size_t>(k1)] - kTileW * t, 0, kTileW);
+            L.tile_row[static_cast<size_t>(t) * (L.R + 1) + k1] = int2{off, cnt};
+            off += 8 * cnt;
+            if (cnt > 0) last = std::max(last, k1);
+        }
+        L.tile_rows[static_cast<size_t>(t)] = last;
+    }
+    L.coef.assign(static_cast<size_t>(off), 0.0);
+    L.row0.assign(static_cast<size_t>(2 * L.J0), 0.0);
+    L.g0.assign(static_cast<size_t>(2 * (L.R + 1)), 0.0);
+    return L;
+}
+
+void lattice_fill(const LatticeHost& s, const PreparedVelocity& v, double* dst) {
+    Grid gr = make_grid(v, true);
+    double* coef = dst;
+    double* row0 = dst + s.coef.size();
+    double* g0 = row0 + s.row0.size();
+    std::fill(dst, dst + s.stride(), 0.0);
+    for (int t = 0; t < s.n_tiles; ++t) {
+        for (int k1 = 1; k1 <= s.R; ++k1) {
+            const int2 tr = s.tile_row[static_cast<size_t>(t) * (s.R + 1) + k1];
+            for (int q = 0; q < tr.y; ++q) {
+                const int j = kTileW * t + q + 1;
+                const Slot gp = gr.at(k1, j), gm = gr.at(k1, -j);
+                const double ar = gp.gr + gm.gr, ai = gp.gi + gm.gi;  // alpha
+                const double br = gp.gr - gm.gr, bi = gp.gi - gm.gi;  // beta
+                double* c = coef + tr.x + 8 * q;
+                // layout matches the kernel's double2 loads (ad_kernels.cu):
+                //   a0 = (c0, c1) -> Ar += c0 r + c1 s
+                //   a1 = (c2, c3) -> Ai += c2 r + c3 s
+                //   b0 = (c4, c5) -> Br += c4 r + c5 s
+                //   b1 = (c6, c7) -> Bi += c6 r + c7 s
+                c[0] = k1 * ar;
+                c[1] = -k1 * bi;
+                c[2] = k1 * ai;
+                c[3] = k1 * br;
+                c[4] = -j * br;
+                c[5] = j * ai;
+                c[6] = -j * bi;
+                c[7] = -j * ar;
+            }
+        }
+    }
+    for (int j = 1; j <= s.J0; ++j) {
+        const Slot g = gr.at(0, j);
+        row0[2 * (j - 1)] = -j * g.gr;
+        row0[2 * (j - 1) + 1] = j * g.gi;
+    }
+    for (int k1 = 1; k1 <= s.R; ++k1) {
+        const Slot g = gr.at(k1, 0);
+        g0[2 * k1] = k1 * g.gr;
+        g0[2 * k1 + 1] = k1 * g.gi;
+    }
+}
+
+std::vector<HostMode> prior_modes(int cutoff) {
+    std::vector<HostMode> out;
+    for (int k1 = -cutoff; k1 <= cutoff; ++k1)
+        for (int k2 = -cutoff; k2 <= cutoff; ++k2) {
+            if (!is_canonical(k1, k2)) continue;
+            if (double(k1) * k1 + double(k2) * k2 > double(cutoff) * cutoff) continue;
+            out.push_back({k1, k2, 0.0, 0.0});
+        }
+    std::sort(out.begin(), out.end(), [](const HostMode& a, const HostMode& b) {
+        const double na = double(a.k1) * a.k1 + double(a.k2) * a.k2;
+        const double nb = double(b.k1) * b.k1 + double(b.k2) * b.k2;
+        if (na != nb) return na < nb;
+        return a.k1 != b.k1 ? a.k1 < b.k1 : a.k2 < b.k2;
+    });
+    return out;
+}
+
+AdObsImg make_ad_obs(double t, double x1, double x2, double dt, double sigma) {
+    AdObsImg o;
+    o.x1 = x1;
+    o.x2 = x2;
+    o.n_steps = static_cast<int64_t>(std::ceil(t / dt));
+    o.dt = dt;
+    o.dt_last = t - double(o.n_steps - 1) * dt;
+    o.rdt = std::sqrt(dt);
+    o.rdt_last = std::sqrt(o.dt_last);
+    o.sr = sigma * o.rdt;
+    o.sr_last = sigma * o.rdt_last;
+    return o;
+}
+
+}  // namespace smc

@@ -1,0 +1,64 @@
+// host_problem.h — host side of the C ABI: validation with the reference's
+// messages, field canonicalisation, step schedules and device-image packing.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/scalarmc_b200.h"
+#include "images.h"
+
+namespace smc {
+
+struct Error {
+    int code;
+    std::string msg;
+};
+[[noreturn]] void raise(int code, const std::string& msg);
+
+// FourierVelocityField after its constructor (src/fields.cpp:35-69).
+struct HostMode {
+    int k1, k2;
+    double re, im;
+};
+struct PreparedVelocity {
+    bool is_constant = true;
+    double c1 = 0.0, c2 = 0.0;
+    int K = 0;
+    std::vector<HostMode> modes;  // canonical, (k1,k2)-sorted
+};
+PreparedVelocity prepare_velocity(const smc_velocity& v);
+double amplitude_bound(const PreparedVelocity& v);  // fields.cpp:109-113, :140-142
+
+void check_kappa(double kappa);                      // fields.cpp:158-160
+void check_scalar(const smc_scalar_field& f);        // fields.cpp:224-232
+void check_domain(const smc_domain& d);              // geometry.cpp:10-19
+
+double ad_resolved_dt(const smc_ad_problem& p);      // forward_ad.cpp:10-15
+void ad_validate(const smc_ad_problem& p);           // forward_ad.cpp:17-28
+double bvp_resolved_dt(const smc_bvp_problem& p, const PreparedVelocity& v);  // forward_bvp.cpp:9-18
+void bvp_validate(const smc_bvp_problem& p);         // forward_bvp.cpp:20-32
+bool domain_contains(const smc_domain& d, double x1, double x2);  // geometry.cpp:22-31
+
+// Lattice coefficients for one coefficient set.
+struct LatticeHost {
+    int K = 0, R = 0, J = 0, J0 = 0, n_tiles = 1;
+    std::vector<int32_t> tile_rows;
+    std::vector<int2> tile_row;
+    std::vector<double> coef, row0, g0;
+    int64_t stride() const { return static_cast<int64_t>(coef.size() + row0.size() + g0.size()); }
+};
+// Structure only (which (k1,k2) slots exist) from a mode list.
+LatticeHost lattice_structure(const PreparedVelocity& v);
+// Fill coefficient values for `v` into a structure built by lattice_structure
+// for the same mode set; writes stride() doubles at dst ([coef|row0|g0]).
+void lattice_fill(const LatticeHost& s, const PreparedVelocity& v, double* dst);
+
+// PriorSpec::modes (src/inference.cpp:24-40).
+std::vector<HostMode> prior_modes(int cutoff);
+
+// Step schedule of one AD observation (sde.cpp:42-45).
+AdObsImg make_ad_obs(double t, double x1, double x2, double dt, double sigma);
+
+}  // namespace smc

@@ -1,0 +1,104 @@
+// kernels.h — launch interface between the host runtime (capi.cu) and the
+// sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "geometry.cuh"
+#include "images.h"
+
+namespace smc {
+
+constexpr int kChunk = 1024;  // == SMC_CHUNK: reduction tree leaf block
+
+// K1: advection-diffusion particles to a fixed time (Algorithm 1;
+// sde.cpp:37-50 + fields.cpp:71-89 + forward_ad.cpp:41-47), one particle per
+// thread.  Grid: x over particle blocks of this shard, y over observations,
+// z over parameter samples.
+struct AdLaunch {
+    VelImg vel;
+    ScalarImg theta0;
+    const AdObsImg* obs;       // [n_obs]
+    int32_t n_obs;
+    uint32_t obs_slot0;        // stream-key obs slot of obs[0] (spec slot, forward_ad.cpp:43)
+    uint64_t seed;             // CRN seed
+    const uint64_t* seeds;     // [n_samples] per-sample seeds, or nullptr (CRN)
+    int64_t n_particles;       // particles per observation
+    int64_t p_begin, p_end;    // this launch's particle range [p_begin, p_end)
+    int32_t n_samples;
+    int32_t precision;         // smc_precision
+    double sigma;              // sqrt(2 kappa)
+    double* values;            // [n_samples][n_obs][p_end - p_begin]
+};
+
+cudaError_t launch_ad_particles(const AdLaunch& L, cudaStream_t s);
+cudaError_t launch_ad_particles_fp32(const AdLaunch& L, cudaStream_t s);
+cudaError_t launch_ad_particles_strict(const AdLaunch& L, cudaStream_t s);
+
+// K2: Dirichlet exit-time walkers (Algorithm 2, PAPER.md:162-178;
+// sde.cpp:52-77 + forward_bvp.cpp:39-46).  Persistent warps: a lane whose
+// walker exits (or fails at max_steps) writes its result and is refilled with
+// the next walker index from a global counter (one atomic per warp refill).
+struct BvpLaunch {
+    VelImg vel;
+    ScalarImg forcing, boundary;
+    DomainImg domain;
+    const double* obs_x;       // [n_obs][2]
+    int32_t n_obs;
+    uint32_t obs_slot0;
+    uint64_t seed;
+    int64_t n_particles;       // walkers per observation launched (particles [0, n))
+    int64_t max_steps;
+    double dt, root_dt, sigma, sr;  // sr = sigma * sqrt(dt)
+    int32_t precision;
+    int32_t pad_;
+    unsigned long long* counter;     // walker queue head (zeroed before launch)
+    unsigned long long* step_total;  // total walker-steps executed (atomicAdd)
+    double* values;            // [n_obs][n_particles]
+    double* aux;               // exit time
+    uint8_t* failed;
+};
+
+cudaError_t launch_bvp_walkers(const BvpLaunch& L, int n_sms, cudaStream_t s);
+cudaError_t launch_bvp_walkers_strict(const BvpLaunch& L, int n_sms, cudaStream_t s);
+
+// Stable compaction of valid walkers per segment (reduce_observation's
+// valid/valid_aux vectors, executor.cpp:93-101).  chunk_tmp: 2 * n_seg *
+// ceil(n/1024) int64.  Writes counts[seg] (valid walkers).
+cudaError_t compact_valid(const double* values, const double* aux, const uint8_t* failed, int64_t n,
+                          int64_t n_seg, double* cvalues, double* caux, int64_t* counts, int64_t* chunk_tmp,
+                          cudaStream_t s);
+
+// K3: deterministic pairwise tree (executor.cpp:11-26) over aligned chunks.
+// One pass turns each segment's n values into ceil(n / 1024) chunk partials.
+//   mode 0: x_i;  mode 1: (x_i - center[seg])^2
+// Out-of-range leaves are -0.0, the exact additive identity.
+cudaError_t launch_tree_pass(const double* in, int64_t in_stride, const int64_t* counts,
+                             int64_t n_uniform, int64_t n_seg, double* out, int64_t out_stride,
+                             const double* center, int mode, cudaStream_t s);
+
+// Runs tree passes until one value per segment remains.  scratch must hold
+// 2 * n_seg * ceil(n/1024) doubles.  counts may be null (all segments n).
+cudaError_t tree_reduce(const double* in, int64_t in_stride, const int64_t* counts, int64_t n,
+                        int64_t n_seg, double* sums, const double* center, int mode,
+                        double* scratch, cudaStream_t s, int* launches);
+
+// means[seg] = sums[seg] / counts[seg]
+cudaError_t launch_divide(const double* sums, const int64_t* counts, int64_t n_uniform, int64_t n_seg,
+                          double* means, cudaStream_t s);
+
+// Finish reduce_observation (executor.cpp:104-116) on device.
+cudaError_t launch_estimates(const double* means, const double* sumsq, const double* sumaux,
+                             const int64_t* counts, int64_t n_uniform, int64_t n_particles,
+                             int64_t n_seg, void* out_estimates, cudaStream_t s);
+
+// Diagnostics / microbenchmarks.
+cudaError_t launch_philox(int64_t n, const uint32_t* ctr, const uint32_t* key, uint32_t* out,
+                          cudaStream_t s);
+cudaError_t launch_normal_pairs(uint64_t seed, uint32_t obs, uint32_t particle, int64_t n,
+                                double* out, cudaStream_t s);
+cudaError_t launch_dfma_peak(int n_blocks, int iters, double* sink, cudaStream_t s);
+
+}  // namespace smc

@@ -1,0 +1,242 @@
+// reduce_kernels.cu — K3: deterministic per-observation reduction
+// (compiled with -fmad=false).
+//
+// Reproduces reduce_observation (src/executor.cpp:87-117) bit for bit given
+// the same per-particle values.  pairwise_sum (executor.cpp:11-26) is an
+// adjacent-pair tree with odd-tail carry; at level L its node i is exactly the
+// sum of the aligned range [i 2^L, min((i+1) 2^L, n)), so it equals a full
+// binary tree over the values padded with -0.0 (x + -0.0 == x for every x,
+// including -0.0).  Each pass sums aligned 1024-leaf chunks: 4 leaves per
+// thread, a shuffle-down tree over the warp (offsets 1..16 pair aligned
+// neighbours), and a fixed 8-way tree over the warps.  Passes compose, so the
+// chunk partials of disjoint particle shards (multi-GPU) finish into the same
+// bits as one device would produce.
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+#include "../../include/scalarmc_b200.h"
+
+namespace smc {
+namespace {
+
+constexpr int kThreads = 256;  // 4 leaves per thread -> 1024-leaf chunk
+
+__global__ void __launch_bounds__(kThreads) tree_pass_kernel(const double* __restrict__ in, int64_t in_stride,
+                                                             const int64_t* __restrict__ counts, int64_t n_uniform,
+                                                             double* __restrict__ out, int64_t out_stride,
+                                                             const double* __restrict__ center, int mode) {
+    const int64_t seg = blockIdx.y;
+    const int64_t n = counts ? counts[seg] : n_uniform;
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kChunk + 4 * threadIdx.x;
+    const double* src = in + seg * in_stride;
+    const double c = (mode == 1) ? center[seg] : 0.0;
+    double leaf[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int64_t i = base + q;
+        if (i < n) {
+            double v = src[i];
+            if (mode == 1) {
+                const double d = v - c;
+                v = d * d;
+            }
+            leaf[q] = v;
+        } else {
+            leaf[q] = -0.0;
+        }
+    }
+    double v = (leaf[0] + leaf[1]) + (leaf[2] + leaf[3]);
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) v = v + __shfl_down_sync(0xffffffffu, v, off);
+    __shared__ double warp_sum[kThreads / 32];
+    if ((threadIdx.x & 31) == 0) warp_sum[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const double* w = warp_sum;
+        out[seg * out_stride + blockIdx.x] = ((w[0] + w[1]) + (w[2] + w[3])) + ((w[4] + w[5]) + (w[6] + w[7]));
+    }
+}
+
+__global__ void divide_kernel(const double* sums, const int64_t* counts, int64_t n_uniform, int64_t n_seg,
+                              double* means) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n_seg) return;
+    const int64_t n = counts ? counts[i] : n_uniform;
+    means[i] = sums[i] / static_cast<double>(n);
+}
+
+__global__ void estimates_kernel(const double* means, const double* sumsq, const double* sumaux,
+                                 const int64_t* counts, int64_t n_uniform, int64_t n_particles, int64_t n_seg,
+                                 smc_estimate* out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n_seg) return;
+    const int64_t nv = counts ? counts[i] : n_uniform;
+    const double n = static_cast<double>(nv);
+    double se = 0.0;
+    if (nv > 1) {
+        const double var = sumsq[i] / (n - 1.0);
+        se = sqrt(var / n);
+    }
+    smc_estimate e;
+    e.mean = means[i];
+    e.std_error = se;
+    e.n_particles = n_particles;
+    e.n_failed = n_particles - nv;
+    e.aux_mean = sumaux ? sumaux[i] / n : 0.0;
+    out[i] = e;
+}
+
+
+// ---- stable compaction of valid walkers (executor.cpp:93-101) -------------
+__global__ void __launch_bounds__(kThreads) count_valid_kernel(const uint8_t* __restrict__ failed, int64_t n,
+                                                               int64_t n_chunks, int64_t* __restrict__ chunk_counts) {
+    const int64_t seg = blockIdx.y;
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kChunk + 4 * threadIdx.x;
+    const uint8_t* f = failed + seg * n;
+    int c = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int64_t i = base + q;
+        if (i < n && !f[i]) ++c;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) c += __shfl_down_sync(0xffffffffu, c, off);
+    __shared__ int wsum[kThreads / 32];
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int k = 0; k < kThreads / 32; ++k) t += wsum[k];
+        chunk_counts[seg * n_chunks + blockIdx.x] = t;
+    }
+}
+
+// Exclusive scan of chunk counts per segment (one thread per segment; at most
+// 2^22 chunks, sequential is fine next to the walkers).
+__global__ void scan_chunks_kernel(const int64_t* chunk_counts, int64_t n_chunks, int64_t n_seg,
+                                   int64_t* chunk_offsets, int64_t* counts) {
+    const int64_t seg = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (seg >= n_seg) return;
+    int64_t acc = 0;
+    for (int64_t c = 0; c < n_chunks; ++c) {
+        chunk_offsets[seg * n_chunks + c] = acc;
+        acc += chunk_counts[seg * n_chunks + c];
+    }
+    counts[seg] = acc;
+}
+
+__global__ void __launch_bounds__(kThreads) compact_kernel(const double* __restrict__ values,
+                                                           const double* __restrict__ aux,
+                                                           const uint8_t* __restrict__ failed, int64_t n,
+                                                           int64_t n_chunks, const int64_t* __restrict__ chunk_offsets,
+                                                           double* __restrict__ cvalues, double* __restrict__ caux) {
+    const int64_t seg = blockIdx.y;
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kChunk + 4 * threadIdx.x;
+    const uint8_t* f = failed + seg * n;
+    bool ok[4];
+    int c = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int64_t i = base + q;
+        ok[q] = i < n && !f[i];
+        c += ok[q];
+    }
+    // block-wide exclusive scan of c (thread order == particle order)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int inc = c;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, off);
+        if (lane >= off) inc += y;
+    }
+    __shared__ int wtot[kThreads / 32];
+    if (lane == 31) wtot[wid] = inc;
+    __syncthreads();
+    int wbase = 0;
+    for (int k = 0; k < wid; ++k) wbase += wtot[k];
+    int64_t pos = chunk_offsets[seg * n_chunks + blockIdx.x] + wbase + (inc - c);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if (ok[q]) {
+            cvalues[seg * n + pos] = values[seg * n + base + q];
+            caux[seg * n + pos] = aux[seg * n + base + q];
+            ++pos;
+        }
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_tree_pass(const double* in, int64_t in_stride, const int64_t* counts, int64_t n_uniform,
+                             int64_t n_seg, double* out, int64_t out_stride, const double* center, int mode,
+                             cudaStream_t s) {
+    // n_uniform is the max count when counts is given.
+    const int64_t chunks = (n_uniform + kChunk - 1) / kChunk;
+    if (chunks <= 0 || n_seg <= 0) return cudaSuccess;
+    const dim3 grid(static_cast<unsigned>(chunks), static_cast<unsigned>(n_seg));
+    tree_pass_kernel<<<grid, kThreads, 0, s>>>(in, in_stride, counts, n_uniform, out, out_stride, center, mode);
+    return cudaGetLastError();
+}
+
+cudaError_t tree_reduce(const double* in, int64_t in_stride, const int64_t* counts, int64_t n, int64_t n_seg,
+                        double* sums, const double* center, int mode, double* scratch, cudaStream_t s,
+                        int* launches) {
+    // Pass 1 reads the leaves (optionally per-segment counts, optional square).
+    int64_t m = (n + kChunk - 1) / kChunk;
+    if (m <= 0) m = 1;
+    double* a = scratch;
+    double* b = scratch + n_seg * m;
+    cudaError_t e;
+    if (n == 0) {
+        // Empty segments sum to +0.0 (pairwise_sum of nothing, executor.cpp:12).
+        return cudaMemsetAsync(sums, 0, sizeof(double) * n_seg, s);
+    }
+    e = launch_tree_pass(in, in_stride, counts, n, n_seg, (m == 1) ? sums : a, (m == 1) ? 1 : m, center, mode, s);
+    if (launches) ++*launches;
+    if (e != cudaSuccess || m == 1) return e;
+    // Later passes: the chunk partials.  Every segment has its own count of
+    // partials when counts are given: ceil(count / 1024); trailing partial
+    // slots beyond it must be excluded (they would be -0.0 anyway, so using
+    // the uniform count is exact).
+    double* cur = a;
+    int64_t len = m;
+    while (len > 1) {
+        const int64_t nxt = (len + kChunk - 1) / kChunk;
+        double* dst = (nxt == 1) ? sums : ((cur == a) ? b : a);
+        e = launch_tree_pass(cur, len, nullptr, len, n_seg, dst, (nxt == 1) ? 1 : nxt, nullptr, 0, s);
+        if (launches) ++*launches;
+        if (e != cudaSuccess) return e;
+        cur = dst;
+        len = nxt;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t launch_divide(const double* sums, const int64_t* counts, int64_t n_uniform, int64_t n_seg,
+                          double* means, cudaStream_t s) {
+    divide_kernel<<<static_cast<unsigned>((n_seg + 127) / 128), 128, 0, s>>>(sums, counts, n_uniform, n_seg, means);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_estimates(const double* means, const double* sumsq, const double* sumaux, const int64_t* counts,
+                             int64_t n_uniform, int64_t n_particles, int64_t n_seg, void* out, cudaStream_t s) {
+    estimates_kernel<<<static_cast<unsigned>((n_seg + 127) / 128), 128, 0, s>>>(
+        means, sumsq, sumaux, counts, n_uniform, n_particles, n_seg, static_cast<smc_estimate*>(out));
+    return cudaGetLastError();
+}
+
+cudaError_t compact_valid(const double* values, const double* aux, const uint8_t* failed, int64_t n, int64_t n_seg,
+                          double* cvalues, double* caux, int64_t* counts, int64_t* chunk_tmp, cudaStream_t s) {
+    const int64_t chunks = (n + kChunk - 1) / kChunk;
+    if (chunks <= 0 || n_seg <= 0) return cudaSuccess;
+    int64_t* chunk_counts = chunk_tmp;
+    int64_t* chunk_offsets = chunk_tmp + n_seg * chunks;
+    const dim3 grid(static_cast<unsigned>(chunks), static_cast<unsigned>(n_seg));
+    count_valid_kernel<<<grid, kThreads, 0, s>>>(failed, n, chunks, chunk_counts);
+    scan_chunks_kernel<<<static_cast<unsigned>((n_seg + 63) / 64), 64, 0, s>>>(chunk_counts, chunks, n_seg,
+                                                                              chunk_offsets, counts);
+    compact_kernel<<<grid, kThreads, 0, s>>>(values, aux, failed, n, chunks, chunk_offsets, cvalues, caux);
+    return cudaGetLastError();
+}
+
+}  // namespace smc

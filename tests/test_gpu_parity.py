@@ -1,0 +1,358 @@
+"""Parity of the CUDA forward map with the reference (GPU, -m gpu).
+
+Every forward map goes through the C ABI (the ctypes mirror in
+paper_1808_10580_b200.api).  Expected values are the golden fixtures made by
+running the real reference (tests/golden/make_golden.py) or, where a fixture
+would be too large, the plain-C oracle on the same inputs.
+
+Tolerances (north_star / SURVEY.md §8(d) parity gate):
+  FP64 means:   |gpu - ref| <= 1e-10 * max(|ref|, theta_scale)
+  FP64 SE:      relative 1e-8
+  FP32 means:   |gpu32 - ref| <= 3 SE_ref (+ the FP64 tolerance)
+Integer / index work (Philox words, counts, n_failed) is bit-exact.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import paper_1808_10580_b200 as S
+import specs
+from conftest import est_from, unhex
+
+pytestmark = pytest.mark.gpu
+
+MEAN_RTOL = 1e-10
+SE_RTOL = 1e-8
+
+
+def theta_scale(field: S.ScalarField) -> float:
+    if field.kind == 1:
+        return sum(abs(t.amplitude) for t in field.terms)
+    return 1.0
+
+
+def assert_estimates(got, ref_list, scale=1.0, exact_counts=True):
+    assert len(got) == len(ref_list)
+    for j, (e, r) in enumerate(zip(got, ref_list)):
+        r = est_from(r) if isinstance(r, dict) else r
+        tol = MEAN_RTOL * max(abs(r["mean"]), scale)
+        assert abs(e.mean - r["mean"]) <= tol, (j, e.mean, r["mean"], abs(e.mean - r["mean"]))
+        assert abs(e.std_error - r["std_error"]) <= SE_RTOL * abs(r["std_error"]) + 1e-300, (j, e.std_error, r["std_error"])
+        assert abs(e.aux_mean - r["aux_mean"]) <= MEAN_RTOL * max(abs(r["aux_mean"]), 1.0)
+        if exact_counts:
+            assert e.n_particles == r["n_particles"] and e.n_failed == r["n_failed"]
+
+
+# ---------------------------------------------------------------- RNG ------
+def test_device_philox_is_bit_exact(ctx, golden):
+    g = golden["philox"]
+    out = S.philox_device(np.array(g["ctr"]), np.array(g["key"]), ctx)
+    assert out.tolist() == g["out"]
+
+
+def test_device_normals_match_reference(ctx, golden):
+    worst = 0.0
+    identical = total = 0
+    for rec in golden["normal_pairs"]:
+        seed, obs, particle = rec["key"]
+        got = S.normal_pairs_device(seed, obs, particle, 64, ctx)
+        want = unhex(rec["pairs"])
+        worst = max(worst, float(np.max(np.abs(got - want))))
+        identical += int(np.sum(got.view(np.uint64) == want.view(np.uint64)))
+        total += got.size
+    assert worst < 1e-14
+    assert identical / total > 0.5  # libdevice vs glibc: equal except in the last ulp
+
+
+# ---------------------------------------------------------------- AD -------
+@pytest.mark.parametrize("precision", [S.Precision.fp64, S.Precision.fp64_strict])
+def test_c1_matches_reference(ctx, golden, precision):
+    g = golden["c1"]
+    spec = specs.c1_two_mode(precision=precision)
+    est = S.observe_ad(spec, 7, ctx=ctx)
+    assert_estimates(est, g["estimates"], theta_scale(spec.initial_condition))
+    assert abs(est[0].mean - (-0.795097030819361)) < 1e-10  # SURVEY.md §8c golden
+
+
+@pytest.mark.parametrize("precision", [S.Precision.fp64, S.Precision.fp64_strict])
+def test_c1_particles_match_reference(ctx, golden, precision):
+    spec = specs.c1_two_mode(precision=precision)
+    same = total = 0
+    for j in range(3):
+        got = S.ad_particle_values(spec, j, 7, 256, ctx)
+        want = unhex(golden["c1"]["particles"][j])
+        assert np.max(np.abs(got - want)) < 1e-12
+        same += int(np.sum(got.view(np.uint64) == want.view(np.uint64)))
+        total += got.size
+    if precision == S.Precision.fp64_strict:
+        # reference operation order: only libm rounding differs
+        assert same / total > 0.2, same / total
+
+
+def test_c2_matches_reference(ctx, golden):
+    g = golden["c2"]
+    u = unhex(g["u"])
+    spec = specs.c2_spec(u, n_particles=g["n_particles"])
+    assert_estimates(S.observe_ad(spec, 808, ctx=ctx), g["estimates"], 1.0)
+    for idx, j in enumerate((0, 4, 8)):
+        got = S.ad_particle_values(spec, j, 808, 128, ctx)
+        assert np.max(np.abs(got - unhex(g["particles"][idx]))) < 1e-11
+
+
+def test_c2_strict_matches_reference(ctx, golden):
+    g = golden["c2"]
+    spec = specs.c2_spec(unhex(g["u"]), n_particles=g["n_particles"], precision=S.Precision.fp64_strict)
+    assert_estimates(S.observe_ad(spec, 808, ctx=ctx), g["estimates"], 1.0)
+
+
+def test_heat_matches_reference_and_analytic(ctx, golden):
+    spec = specs.heat_spec(0.01, 0.5, (0.0, 0.0), 20000, 1e-3)
+    est = S.observe_ad(spec, 20240501, ctx=ctx)
+    assert_estimates(est, golden["heat"]["estimates"], 1.0)
+    target = math.exp(-4.0 * math.pi ** 2 * 0.01 * 0.5)  # acceptance.cpp:42
+    assert abs(est[0].mean - target) <= 3.0 * est[0].std_error + 0.01
+
+
+def test_batched_matches_reference_per_sample(ctx, golden):
+    g = golden["c4"]
+    U = unhex(g["U"])
+    base = specs.c4_base(n_particles=g["n_particles"])
+    out = S.observe_ad_batched(base, specs.C4_PRIOR, U, 808, ctx=ctx)
+    for b in range(U.shape[0]):
+        got = [S.ParticleEstimate(*[out[b, j][k] for k in out.dtype.names]) for j in range(out.shape[1])]
+        assert_estimates(got, g["estimates"][b], 1.0)
+
+
+def test_batched_equals_single_calls(ctx):
+    rng = np.random.default_rng(1)
+    prior = S.PriorSpec(4, 1.0, 2.0)
+    U = rng.normal(size=(5, prior.dimension())) * 0.3
+    base = specs.c4_base(n_particles=300)
+    out = S.observe_ad_batched(base, prior, U, 99, ctx=ctx)
+    for b in range(5):
+        spec = specs.c4_base(n_particles=300)
+        spec.velocity = S.VelocityField.fourier(S.velocity_from_coefficients(prior, U[b]))
+        single = S.observe_ad(spec, 99, ctx=ctx)
+        for j, e in enumerate(single):
+            assert out[b, j]["mean"] == e.mean and out[b, j]["std_error"] == e.std_error
+
+
+def test_batched_per_sample_seeds(ctx):
+    prior = S.PriorSpec(3, 1.0, 2.0)
+    U = np.tile(np.random.default_rng(2).normal(size=prior.dimension()) * 0.2, (3, 1))
+    base = specs.c4_base(n_particles=256)
+    crn = S.observe_ad_batched(base, prior, U, 5, ctx=ctx)
+    assert np.array_equal(crn["mean"][0], crn["mean"][1])
+    seeded = S.observe_ad_batched(base, prior, U, 5, seeds=np.array([5, 6, 7], dtype=np.uint64), ctx=ctx)
+    assert np.array_equal(seeded["mean"][0], crn["mean"][0])
+    assert not np.array_equal(seeded["mean"][1], crn["mean"][1])
+
+
+def test_misfit_matches_reference(ctx, golden):
+    g = golden["misfit"]
+    prior = S.PriorSpec(2, 0.6, 2.5)
+    fwd = specs.c4_base(n_particles=160)
+    fwd.dt = 0.006
+    like = S.LikelihoodSpec(data=g["data"], noise_std=g["noise_std"], forward=fwd, forward_seed=g["forward_seed"])
+    phi = like.misfit(prior, unhex(g["u"]))
+    ref = float.fromhex(g["phi"])
+    assert abs(phi - ref) <= 1e-9 * max(abs(ref), 1.0)
+    assert abs(like.misfit_batched(prior, unhex(g["u"])[None, :])[0] - ref) <= 1e-9 * max(abs(ref), 1.0)
+
+
+# ------------------------------------------- reference unit tests, on GPU ----
+def test_zero_diffusion_is_exact(ctx):
+    # test_forward.cpp:34-47
+    spec = S.AdProblemSpec(diffusion=S.DiffusionModel.isotropic(0.0),
+                           initial_condition=S.ScalarField.cosine_mode(1, 0, 1.0), n_particles=4096,
+                           observations=[S.AdObservation(0.5, S.Vec2(0.0, 0.25)),
+                                         S.AdObservation(1.0, S.Vec2(0.125, 0.5))])
+    for prec in (S.Precision.fp64, S.Precision.fp64_strict):
+        spec.precision = prec
+        est = S.observe_ad(spec, 1, ctx=ctx)
+        for j, o in enumerate(spec.observations):
+            assert est[j].mean == spec.initial_condition(o.x)
+            assert est[j].std_error == 0.0
+
+
+def test_single_slot_equivalence_and_determinism(ctx):
+    # test_forward.cpp:59-82
+    spec = specs.heat_spec(0.02, 0.25, (0.0, 0.0), 2000, 2e-3)
+    spec.observations += [S.AdObservation(0.5, S.Vec2(0.25, 0.75)), S.AdObservation(0.6, S.Vec2(0.5, 0.5))]
+    full = S.observe_ad(spec, 5, ctx=ctx)
+    for j in range(3):
+        single = S.observe_ad_single(spec, j, 5, ctx=ctx)
+        assert single == full[j]
+    with pytest.raises(IndexError):
+        S.observe_ad_single(spec, 3, 5, ctx=ctx)
+    truncated = specs.heat_spec(0.02, 0.25, (0.0, 0.0), 2000, 2e-3)
+    truncated.observations += [S.AdObservation(0.5, S.Vec2(0.25, 0.75))]
+    part = S.observe_ad(truncated, 5, ctx=ctx)
+    assert part[0] == full[0] and part[1] == full[1]
+    assert S.observe_ad(spec, 5, ctx=ctx) == full
+
+
+def test_linearity_in_theta0(ctx):
+    # test_forward.cpp:84-94
+    base = specs.heat_spec(0.03, 0.2, (0.3, 0.6), 3000, 1e-3)
+    base.initial_condition = S.ScalarField.cosine_mode(1, 1, 1.0, 0.4)
+    scaled = specs.heat_spec(0.03, 0.2, (0.3, 0.6), 3000, 1e-3)
+    scaled.initial_condition = S.ScalarField.cosine_series([(-2.5, (2 * math.pi, 2 * math.pi), 0.4),
+                                                            (1.25, (0.0, 0.0), 0.0)])
+    g = S.observe_ad(base, 21, ctx=ctx)[0]
+    h = S.observe_ad(scaled, 21, ctx=ctx)[0]
+    assert abs(h.mean - (-2.5 * g.mean + 1.25)) <= 1e-12 * abs(-2.5 * g.mean + 1.25)
+
+
+def test_maximum_principle_property(ctx):
+    # acceptance.cpp:362-406, 200 random configurations, N_p = 32
+    rng = np.random.default_rng(4096)
+    violations = 0
+    for trial in range(200):
+        f = specs.random_fourier(rng, int(rng.integers(1, 4)), 3)
+        c, a = 4 * rng.random() - 2, 2 * rng.random() - 1
+        tk1, tk2 = (int(v) for v in rng.integers(-3, 4, size=2))
+        if tk1 == 0 and tk2 == 0:
+            tk1 = 1
+        t = 0.05 + 0.25 * rng.random()
+        spec = S.AdProblemSpec(velocity=S.VelocityField.fourier(f),
+                               diffusion=S.DiffusionModel.isotropic(0.1 * rng.random()),
+                               initial_condition=S.ScalarField.cosine_series(
+                                   [(a, (2 * math.pi * tk1, 2 * math.pi * tk2), 0.0), (c, (0.0, 0.0), 0.0)]),
+                               observations=[S.AdObservation(t, S.Vec2(rng.random(), rng.random()))],
+                               dt=t / 20.0, n_particles=32)
+        m = S.observe_ad(spec, 5000 + trial, ctx=ctx)[0].mean
+        violations += not (c - abs(a) <= m <= c + abs(a))
+    assert violations == 0
+
+
+def test_validation_errors_on_device_path(ctx):
+    spec = S.AdProblemSpec()
+    with pytest.raises(ValueError, match="no observations"):
+        S.observe_ad(spec, 0, ctx=ctx)
+    spec.observations = [S.AdObservation(0.0, S.Vec2(0.5, 0.5))]
+    with pytest.raises(ValueError, match="times must be positive"):
+        S.observe_ad(spec, 0, ctx=ctx)
+    spec.observations = [S.AdObservation(0.5, S.Vec2(1.5, 0.5))]
+    with pytest.raises(ValueError, match=r"\[0,1\)\^2"):
+        S.observe_ad(spec, 0, ctx=ctx)
+
+
+# ------------------------------------------------ sharded (multi-GPU) path ----
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_sharded_partials_are_bit_identical(ctx, world):
+    from paper_1808_10580_b200 import distributed as D
+    u = S.prior_draw(specs.C2_PRIOR, 808, 0xBE9C4, 0, ctx)
+    spec = specs.c2_spec(u, n_particles=5000)
+    spec.observations = spec.observations[:3]
+    spec.observations = [S.AdObservation(0.2, o.x) for o in spec.observations]
+    whole = S.observe_ad(spec, 808, ctx=ctx)
+    est = D.observe_ad_emulated(spec, 808, world, ctx)
+    for a, b in zip(whole, est):
+        assert a.mean == b.mean and a.std_error == b.std_error
+
+
+# ---------------------------------------------------------------- FP32 -----
+def test_fp32_within_three_standard_errors(ctx, golden):
+    spec = specs.c1_two_mode(n_particles=10000, precision=S.Precision.fp32)
+    est = S.observe_ad(spec, 7, ctx=ctx)
+    for e, r in zip(est, golden["c1"]["estimates"]):
+        r = est_from(r)
+        assert abs(e.mean - r["mean"]) <= 3.0 * r["std_error"]
+    u = unhex(golden["c2"]["u"])
+    spec2 = specs.c2_spec(u, n_particles=512, precision=S.Precision.fp32)
+    for e, r in zip(S.observe_ad(spec2, 808, ctx=ctx), golden["c2"]["estimates"]):
+        r = est_from(r)
+        assert abs(e.mean - r["mean"]) <= 3.0 * r["std_error"]
+
+
+# ---------------------------------------------------------------- BVP ------
+def test_bvp_box_matches_reference(ctx, golden):
+    g = golden["bvp_box"]
+    spec = specs.paper_bvp()
+    est = S.observe_bvp(spec, 606, ctx=ctx)
+    assert_estimates(est, g["estimates"], 1.0)
+    vals, aux, failed = S.bvp_particle_values(spec, 0, 606, 256, ctx)
+    p = g["particles"]
+    assert failed.tolist() == p["failed"]
+    assert np.max(np.abs(vals - unhex(p["values"]))) < 1e-11
+    assert np.max(np.abs(aux - unhex(p["aux"]))) < 1e-12
+
+
+def test_bvp_strict_matches_reference(ctx, golden):
+    spec = specs.paper_bvp(precision=S.Precision.fp64_strict)
+    assert_estimates(S.observe_bvp(spec, 606, ctx=ctx), golden["bvp_box"]["estimates"], 1.0)
+
+
+def test_c3_shape_matches_reference(ctx, golden):
+    assert_estimates(S.observe_bvp(specs.c3_spec(n_particles=512), 606, ctx=ctx), golden["c3"]["estimates"], 1.0)
+
+
+def test_bvp_disk_fourier_matches_reference(ctx, golden):
+    disk = specs.paper_bvp(n_particles=1000, amplitudes=(1.0, -0.5, 2.0), observations=[(0.5, 0.5), (0.3, 0.6)],
+                           velocity=S.VelocityField.fourier(specs.random_fourier(np.random.default_rng(5), 6, 3)))
+    disk.domain = S.Domain.disk((0.5, 0.5), 0.5)
+    disk.dt = 5e-4
+    assert_estimates(S.observe_bvp(disk, 5, ctx=ctx), golden["bvp_disk"]["estimates"], 1.0)
+
+
+def test_bvp_max_steps_failures_excluded(ctx, golden):
+    fail = specs.paper_bvp(n_particles=300, observations=[(0.94, 0.94), (0.8, 0.5)])
+    fail.max_steps = 300
+    assert_estimates(S.observe_bvp(fail, 77, ctx=ctx), golden["bvp_maxsteps"]["estimates"], 1.0)
+    fail.observations = [(0.5, 0.5)]
+    fail.max_steps = 5
+    with pytest.raises(RuntimeError, match="every particle of an observation failed"):
+        S.observe_bvp(fail, 77, ctx=ctx)
+
+
+def test_bvp_constant_boundary_exact(ctx):
+    # test_forward.cpp:112-126
+    spec = S.BvpProblemSpec(diffusion=S.DiffusionModel.isotropic(0.2), boundary_data=S.ScalarField.constant(3.5),
+                            observations=[(0.5, 0.5), (0.25, 0.7)], n_particles=1024, dt=1e-3)
+    for e in S.observe_bvp(spec, 9, ctx=ctx):
+        assert e.mean == 3.5 and e.std_error == 0.0 and e.aux_mean > 0.0 and e.n_failed == 0
+
+
+def test_bvp_manufactured_solution(ctx):
+    # test_forward.cpp:128-141 / acceptance.cpp:88-104
+    spec = S.BvpProblemSpec(velocity=S.VelocityField.constant((1.0, 1.0)), diffusion=S.DiffusionModel.isotropic(0.25),
+                            forcing=S.ScalarField.constant(-2.0), boundary_data=S.ScalarField.affine(0.0, (1.0, 1.0)),
+                            observations=[(0.5, 0.5)], n_particles=100000, dt=2e-4)
+    e = S.observe_bvp(spec, 31415, ctx=ctx)[0]
+    assert abs(e.mean - 1.0) <= 3.0 * e.std_error + 0.01
+
+
+def test_bvp_linearity(ctx):
+    # test_forward.cpp:143-164
+    h = math.pi / 2
+    spec = S.BvpProblemSpec(velocity=S.VelocityField.constant((0.5, -0.25)), diffusion=S.DiffusionModel.isotropic(0.15),
+                            forcing=S.ScalarField.gaussian_bumps([(1.0, (0.4, 0.4))], 4.0),
+                            boundary_data=S.ScalarField.cosine_series([(0.5, (h, 0.0), 0.0), (0.5, (0.0, h), 0.0)]),
+                            observations=[(0.5, 0.5), (0.3, 0.8)], n_particles=2000, dt=5e-4)
+    a = -3.0
+    scaled = S.BvpProblemSpec(velocity=spec.velocity, diffusion=spec.diffusion,
+                              forcing=spec.forcing.with_bump_amplitudes([a]),
+                              boundary_data=S.ScalarField.cosine_series([(a * 0.5, (h, 0.0), 0.0),
+                                                                         (a * 0.5, (0.0, h), 0.0)]),
+                              observations=spec.observations, n_particles=2000, dt=5e-4)
+    for b, m in zip(S.observe_bvp(spec, 17, ctx=ctx), S.observe_bvp(scaled, 17, ctx=ctx)):
+        assert abs(m.mean - a * b.mean) <= 1e-12 * abs(a * b.mean)
+
+
+def test_forcing_cost_matches_reference(ctx, golden):
+    for rec in golden["forcing_cost"]:
+        control = S.ForcingControl(initial_amplitudes=rec["F"], centers=[(0.68, 0.4), (0.4, 0.68), (0.82, 0.82)],
+                                   sharpness=4.0, target=rec["target"],
+                                   observation_points=[(0.88, 0.6), (0.6, 0.88), (0.94, 0.94)])
+        cost = S.forcing_cost(rec["F"], control, specs.paper_bvp(n_particles=400), rec["seed"])
+        ref = float.fromhex(rec["cost"])
+        assert abs(cost - ref) <= 1e-9 * max(ref, 1.0)
+
+
+def test_bvp_fp32_within_three_standard_errors(ctx, golden):
+    spec = specs.paper_bvp(precision=S.Precision.fp32)
+    for e, r in zip(S.observe_bvp(spec, 606, ctx=ctx), golden["bvp_box"]["estimates"]):
+        r = est_from(r)
+        assert abs(e.mean - r["mean"]) <= 3.0 * r["std_error"]
