@@ -94,7 +94,8 @@ def build_workload(name: str, ctx):
                 "modes": M, "n_obs": 64, "particles_per_obs": 32768, "seed": 808}
     else:
         raise SystemExit(f"unknown config {name}")
-    steps = sum(int(math.ceil(o.t / spec.dt)) for o in spec.observations) * spec.n_particles
+    dt = spec.resolved_dt()
+    steps = sum(int(math.ceil(o.t / dt)) for o in spec.observations) * spec.n_particles
     return spec, steps, flops_ad(K, M), desc
 
 

@@ -1,0 +1,80 @@
+// ad_body.cuh — the per-particle loop of K1, shared by the generic-lattice
+// kernel (ad_kernels.cu) and the compile-time disk kernels (ad_disk.cu).
+//
+// Each thread owns P particles of one observation for their whole paths
+// (Algorithm 1): Philox block -> Box-Muller -> velocity ->
+// Euler-Maruyama step -> torus wrap, n_j times in registers, then theta_0 at
+// the terminal point (simulate_to_time, src/sde.cpp:37-50; work lambda,
+// src/forward_ad.cpp:41-47).  Only the terminal values touch HBM.  With P > 1
+// the velocity evaluator loads each coefficient once for all P particles.
+#pragma once
+
+#include "kernels.h"
+#include "scalar_eval.cuh"
+#include "smc_device.cuh"
+#include "velocity.cuh"
+
+namespace smc {
+
+__device__ __forceinline__ double log_t(double x) { return log(x); }
+__device__ __forceinline__ float log_t(float x) { return __logf(x); }
+
+// Particles local[p] (p < P) of observation `obs`; entries >= span are
+// computed on a clamped index and not stored.
+template <class T, int P, class Vel>
+__device__ __forceinline__ void ad_particles_p(const AdLaunch& L, int obs, int sample, const int64_t (&local)[P],
+                                               int64_t span, Vel&& velocity) {
+    const AdObsImg o = L.obs[obs];
+    const uint64_t seed = L.seeds ? __ldg(L.seeds + sample) : L.seed;
+    const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
+    const uint32_t slot = L.obs_slot0 + obs;
+    uint32_t particle[P];
+    T x1[P], x2[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        particle[p] = static_cast<uint32_t>(L.p_begin + (local[p] < span ? local[p] : span - 1));
+        x1[p] = T(o.x1 - floor(o.x1));
+        x2[p] = T(o.x2 - floor(o.x2));
+    }
+    const T dt = T(o.dt), dt_last = T(o.dt_last), sr = T(o.sr), sr_last = T(o.sr_last);
+    const int64_t n = o.n_steps;
+    for (int64_t step = 0; step < n; ++step) {
+        T xi1[P], xi2[P], v1[P], v2[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const Uniform2 u = uniform_block(k0, k1, slot, particle[p], static_cast<uint64_t>(step));
+            const T rad = sqrt(T(-2) * log_t(T(u.u0)));
+            T sn, cs;
+            sincospi_t(T(2) * T(u.u1), &sn, &cs);
+            xi1[p] = rad * cs;
+            xi2[p] = rad * sn;
+        }
+        velocity(x1, x2, v1, v2);
+        const bool last = step + 1 == n;
+        const T h = last ? dt_last : dt;
+        const T s = last ? sr_last : sr;
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            x1[p] = fma(s, xi1[p], fma(-v1[p], h, x1[p]));
+            x2[p] = fma(s, xi2[p], fma(-v2[p], h, x2[p]));
+            x1[p] -= floor(x1[p]);
+            x2[p] -= floor(x2[p]);
+        }
+    }
+    double* out = L.values + (static_cast<int64_t>(sample) * L.n_obs + obs) * span;
+#pragma unroll
+    for (int p = 0; p < P; ++p)
+        if (local[p] < span) out[local[p]] = scalar_eval(L.theta0, double(x1[p]), double(x2[p]));
+}
+
+// Single-particle convenience wrapper.
+template <class T, class Vel>
+__device__ __forceinline__ void ad_particle(const AdLaunch& L, int obs, int sample, int64_t local, int64_t span,
+                                            Vel&& velocity) {
+    const int64_t loc[1] = {local};
+    ad_particles_p<T, 1>(L, obs, sample, loc, span, [&](const T (&x1)[1], const T (&x2)[1], T (&v1)[1], T (&v2)[1]) {
+        velocity(x1[0], x2[0], v1[0], v2[0]);
+    });
+}
+
+}  // namespace smc

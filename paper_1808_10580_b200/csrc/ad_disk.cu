@@ -1,0 +1,262 @@
+// ad_disk.cu — K1 specialised at compile time for the full Fourier disk
+// |k| <= K (K = 1..kDiskMaxK).
+//
+// The lattice velocity with every loop bound known: the
+// powers P2[j] = e^{2 pi i j x2} and Q[j] = j P2[j] live in registers, each
+// row's +/-j pairs unroll into 8 DFMAs on 4 coefficients, and every row folds
+// into v through P1[k1] = e^{2 pi i k1 x1}.  Coefficients are staged once per
+// block in shared memory and read with broadcast vector loads at compile-time
+// offsets, each load feeding all P particles of the thread.  Modes absent from
+// the caller's field are zero coefficients; the host only picks this kernel
+// when the field fills most of its disk.
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <utility>
+
+#include "ad_body.cuh"
+#include "disk_shape.h"
+
+namespace smc {
+namespace {
+
+constexpr int kBlock = 128;
+
+template <int K, class T>
+struct DiskCoef {
+    T c[DiskShape<K>::n_coef];
+};
+
+// Coefficients staged in shared memory, read with volatile vector loads at
+// compile-time offsets: one LDS.128 (broadcast) per two coefficients, kept
+// inside the step loop (3-6 KB of loop-invariant values cannot live in
+// registers, and hoisting part of them only produces register shuffles).
+template <class T>
+struct SmemCoef {
+    uint32_t base;
+    template <int O>
+    __device__ __forceinline__ void get2(T& a, T& b) const;
+};
+template <>
+template <int O>
+__device__ __forceinline__ void SmemCoef<double>::get2(double& a, double& b) const {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2+%3];" : "=d"(a), "=d"(b) : "r"(base), "n"(O * 8));
+}
+template <>
+template <int O>
+__device__ __forceinline__ void SmemCoef<float>::get2(float& a, float& b) const {
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2+%3];" : "=f"(a), "=f"(b) : "r"(base), "n"(O * 4));
+}
+
+template <int K, class T, int P>
+struct Powers {
+    T pr[P][K + 1], pi[P][K + 1];  // P2[j]
+    T qr[P][K + 1], qi[P][K + 1];  // Q[j] = j P2[j]
+};
+
+template <int P, class T>
+struct RowAcc {
+    T Ar[P], Ai[P], Br[P], Bi[P];
+};
+
+// One (k1, +/-j) pair, alpha = g(k1,j) + g(k1,-j), beta = g(k1,j) - g(k1,-j):
+//   A  += (ar r - bi s) + i (ai r + br s)
+//   B' += (br qr - ai qs) + i (bi qr + ar qs)
+template <int K, int K1, int J, class T, int P>
+__device__ __forceinline__ void disk_pair(const SmemCoef<T>& C, const Powers<K, T, P>& W, RowAcc<P, T>& a) {
+    constexpr int o = 4 * (DiskShape<K>::pair_offset(K1) + J - 1);
+    T ar, ai, br, bi;
+    C.template get2<o>(ar, ai);
+    C.template get2<o + 2>(br, bi);
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        a.Ar[p] = fma(ar, W.pr[p][J], a.Ar[p]);
+        a.Ai[p] = fma(ai, W.pr[p][J], a.Ai[p]);
+        a.Br[p] = fma(br, W.qr[p][J], a.Br[p]);
+        a.Bi[p] = fma(bi, W.qr[p][J], a.Bi[p]);
+        a.Ar[p] = fma(bi, -W.pi[p][J], a.Ar[p]);
+        a.Ai[p] = fma(br, W.pi[p][J], a.Ai[p]);
+        a.Br[p] = fma(ai, -W.qi[p][J], a.Br[p]);
+        a.Bi[p] = fma(ar, W.qi[p][J], a.Bi[p]);
+    }
+}
+
+template <int K, int K1, class T, int P, int... Js>
+__device__ __forceinline__ void disk_row_pairs(const SmemCoef<T>& C, const Powers<K, T, P>& W, RowAcc<P, T>& a,
+                                               std::integer_sequence<int, Js...>) {
+    (disk_pair<K, K1, Js + 1, T, P>(C, W, a), ...);
+}
+
+// Row k1 >= 1: P1 <- P1 e1 (k1 > 1), row sums A and B', then
+//   v2 += k1 Re(P1 A),  v1 -= Re(P1 B').
+template <int K, int K1, class T, int P>
+__device__ __forceinline__ void disk_row(const SmemCoef<T>& C, const Powers<K, T, P>& W, const T (&c1)[P],
+                                         const T (&s1)[P], T (&p1r)[P], T (&p1i)[P], T (&acc1)[P], T (&acc2)[P]) {
+    using S = DiskShape<K>;
+    if constexpr (K1 > 1) {
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const T nr = fma(p1r[p], c1[p], -p1i[p] * s1[p]);
+            p1i[p] = fma(p1r[p], s1[p], p1i[p] * c1[p]);
+            p1r[p] = nr;
+        }
+    }
+    T g0r, g0i;
+    C.template get2<S::g0_offset + 2 * (K1 - 1)>(g0r, g0i);
+    RowAcc<P, T> a;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        a.Ar[p] = g0r;
+        a.Ai[p] = g0i;
+        a.Br[p] = T(0);
+        a.Bi[p] = T(0);
+    }
+    disk_row_pairs<K, K1, T, P>(C, W, a, std::make_integer_sequence<int, S::jmax(K1)>{});
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        acc2[p] = fma(T(K1), fma(p1r[p], a.Ar[p], -p1i[p] * a.Ai[p]), acc2[p]);
+        acc1[p] = fma(-p1r[p], a.Br[p], fma(p1i[p], a.Bi[p], acc1[p]));
+    }
+}
+
+template <int K, class T, int P, int... K1s>
+__device__ __forceinline__ void disk_rows(const SmemCoef<T>& C, const Powers<K, T, P>& W, const T (&c1)[P],
+                                          const T (&s1)[P], T (&acc1)[P], T (&acc2)[P],
+                                          std::integer_sequence<int, K1s...>) {
+    T p1r[P], p1i[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        p1r[p] = c1[p];
+        p1i[p] = s1[p];
+    }
+    (disk_row<K, K1s + 1, T, P>(C, W, c1, s1, p1r, p1i, acc1, acc2), ...);
+}
+
+// Row k1 = 0: modes (0, j) only (g- = 0), P1 = 1: v1 = -sum (g_re qr - g_im qs).
+template <int K, int J, class T, int P>
+__device__ __forceinline__ void disk_row0_term(const SmemCoef<T>& C, const Powers<K, T, P>& W, T (&a0)[P],
+                                               T (&a1)[P]) {
+    T gr, gi;
+    C.template get2<DiskShape<K>::row0_offset + 2 * J>(gr, gi);
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        a0[p] = fma(gr, -W.qr[p][J + 1], a0[p]);
+        a1[p] = fma(gi, W.qi[p][J + 1], a1[p]);
+    }
+}
+
+template <int K, class T, int P, int... Js>
+__device__ __forceinline__ void disk_row0(const SmemCoef<T>& C, const Powers<K, T, P>& W, T (&acc1)[P],
+                                          std::integer_sequence<int, Js...>) {
+    T a0[P], a1[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) a0[p] = a1[p] = T(0);
+    (disk_row0_term<K, Js, T, P>(C, W, a0, a1), ...);
+#pragma unroll
+    for (int p = 0; p < P; ++p) acc1[p] = a0[p] + a1[p];
+}
+
+template <int K, class T, int P>
+__device__ __forceinline__ void velocity_disk(const SmemCoef<T>& C, const T (&x1)[P], const T (&x2)[P], T (&v1)[P],
+                                              T (&v2)[P]) {
+    T s1[P], c1[P];
+    Powers<K, T, P> W;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        T s2, c2;
+        sincospi_t(T(2) * x1[p], &s1[p], &c1[p]);
+        sincospi_t(T(2) * x2[p], &s2, &c2);
+        W.pr[p][1] = c2;
+        W.pi[p][1] = s2;
+#pragma unroll
+        for (int j = 2; j <= K; ++j) {
+            W.pr[p][j] = fma(W.pr[p][j - 1], c2, -W.pi[p][j - 1] * s2);
+            W.pi[p][j] = fma(W.pr[p][j - 1], s2, W.pi[p][j - 1] * c2);
+        }
+        W.qr[p][1] = c2;
+        W.qi[p][1] = s2;
+#pragma unroll
+        for (int j = 2; j <= K; ++j) {
+            W.qr[p][j] = T(j) * W.pr[p][j];
+            W.qi[p][j] = T(j) * W.pi[p][j];
+        }
+    }
+    T acc1[P], acc2[P];
+    disk_row0<K, T, P>(C, W, acc1, std::make_integer_sequence<int, K>{});
+#pragma unroll
+    for (int p = 0; p < P; ++p) acc2[p] = T(0);
+    disk_rows<K, T, P>(C, W, c1, s1, acc1, acc2, std::make_integer_sequence<int, K>{});
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        v1[p] = acc1[p];
+        v2[p] = acc2[p];
+    }
+}
+
+template <int K, class T, int P>
+__global__ void __launch_bounds__(kBlock) ad_particles_disk(const AdLaunch L, const DiskCoef<K, T> Pc) {
+    __shared__ __align__(16) T staged[DiskShape<K>::n_coef];
+    for (int i = threadIdx.x; i < DiskShape<K>::n_coef; i += kBlock) staged[i] = Pc.c[i];
+    __syncthreads();
+    const SmemCoef<T> C{static_cast<uint32_t>(__cvta_generic_to_shared(staged))};
+    const int obs = blockIdx.y;
+    const int64_t span = L.p_end - L.p_begin;
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kBlock * P + threadIdx.x;
+    if (base >= span) return;
+    int64_t local[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) local[p] = base + static_cast<int64_t>(p) * kBlock;
+    ad_particles_p<T, P>(L, obs, 0, local, span,
+                         [&](const T (&x1)[P], const T (&x2)[P], T (&v1)[P], T (&v2)[P]) {
+                             velocity_disk<K, T, P>(C, x1, x2, v1, v2);
+                         });
+}
+
+template <int K, class T, int P>
+cudaError_t launch_k(const AdLaunch& L, const double* host_coef, cudaStream_t s) {
+    DiskCoef<K, T> C;
+    for (int i = 0; i < DiskShape<K>::n_coef; ++i) C.c[i] = static_cast<T>(host_coef[i]);
+    const int64_t span = L.p_end - L.p_begin;
+    const int64_t per_block = static_cast<int64_t>(kBlock) * P;
+    const dim3 grid(static_cast<unsigned>((span + per_block - 1) / per_block), static_cast<unsigned>(L.n_obs), 1);
+    ad_particles_disk<K, T, P><<<grid, kBlock, 0, s>>>(L, C);
+    return cudaGetLastError();
+}
+
+template <class T, int P>
+cudaError_t dispatch_p(const AdLaunch& L, int K, const double* c, cudaStream_t s) {
+    switch (K) {
+        case 1: return launch_k<1, T, P>(L, c, s);
+        case 2: return launch_k<2, T, P>(L, c, s);
+        case 3: return launch_k<3, T, P>(L, c, s);
+        case 4: return launch_k<4, T, P>(L, c, s);
+        case 5: return launch_k<5, T, P>(L, c, s);
+        case 6: return launch_k<6, T, P>(L, c, s);
+        case 7: return launch_k<7, T, P>(L, c, s);
+        case 8: return launch_k<8, T, P>(L, c, s);
+        case 9: return launch_k<9, T, P>(L, c, s);
+        case 10: return launch_k<10, T, P>(L, c, s);
+        case 11: return launch_k<11, T, P>(L, c, s);
+        case 12: return launch_k<12, T, P>(L, c, s);
+        default: return cudaErrorNotSupported;
+    }
+}
+
+// Particles per thread: 2 for FP64 (each staged coefficient load feeds two
+// particles), overridable with SMC_DISK_P=1|2 for experiments.
+template <class T>
+cudaError_t dispatch(const AdLaunch& L, int K, const double* c, cudaStream_t s) {
+    const char* e = std::getenv("SMC_DISK_P");
+    const int P = (e && std::atoi(e) > 0) ? std::atoi(e) : 2;
+    return P == 1 ? dispatch_p<T, 1>(L, K, c, s) : dispatch_p<T, 2>(L, K, c, s);
+}
+
+}  // namespace
+
+cudaError_t launch_ad_disk(const AdLaunch& L, int K, const double* host_coef, cudaStream_t s) {
+    if (L.p_end - L.p_begin <= 0) return cudaSuccess;
+    if (L.n_samples != 1) return cudaErrorNotSupported;
+    return L.precision == 1 ? dispatch<float>(L, K, host_coef, s) : dispatch<double>(L, K, host_coef, s);
+}
+
+}  // namespace smc

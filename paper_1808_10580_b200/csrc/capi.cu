@@ -11,12 +11,14 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
 #include <vector>
 
 #include "../../include/scalarmc_b200.h"
+#include "disk_shape.h"
 #include "host_problem.h"
 #include "kernels.h"
 
@@ -241,6 +243,8 @@ VelImg patch(const VelRef& r, unsigned char* base) {
 // Everything a K1 launch needs, prepared and uploaded.
 struct AdPrepared {
     AdLaunch L{};
+    int disk_K = 0;            // > 0: use the compile-time disk kernel
+    std::vector<double> disk;  // its coefficient block
     int64_t n_obs = 0;
     int64_t steps_per_particle_sum = 0;  // sum_j n_j
 };
@@ -279,11 +283,21 @@ AdPrepared prepare_ad(smc_ctx* ctx, const smc_ad_problem& p, const std::vector<c
     L.precision = p.precision;
     L.sigma = sigma;
     out.n_obs = obs_count;
+    // Dense fields with K <= kDiskMaxK take the compile-time disk kernel.
+    if (!structure.is_constant && fills.size() == 1 && p.precision != SMC_FP64_STRICT && structure.K <= kDiskMaxK &&
+        2 * structure.modes.size() >= static_cast<size_t>(disk_n_modes(structure.K)) &&
+        std::getenv("SMC_DISABLE_DISK") == nullptr) {
+        out.disk_K = structure.K;
+        out.disk.resize(static_cast<size_t>(disk_n_coef(structure.K)));
+        disk_fill(structure.K, *fills[0], out.disk.data());
+    }
     return out;
 }
 
-void run_particles(smc_ctx* ctx, AdLaunch& L) {
-    if (L.precision == SMC_FP64_STRICT) {
+void run_particles(smc_ctx* ctx, AdLaunch& L, const AdPrepared* P = nullptr) {
+    if (P && P->disk_K > 0 && L.n_samples == 1) {
+        CK(launch_ad_disk(L, P->disk_K, P->disk.data(), ctx->stream));
+    } else if (L.precision == SMC_FP64_STRICT) {
         if (L.n_samples != 1) raise(SMC_EINVAL, "strict precision is single-sample only");
         if (!L.vel.is_constant && L.vel.K > 128) raise(SMC_EINVAL, "strict precision supports max_wavenumber <= 128");
         CK(launch_ad_particles_strict(L, ctx->stream));
@@ -338,7 +352,7 @@ void ad_observe_range(smc_ctx* ctx, const smc_ad_problem& p, uint64_t seed, int6
     const int64_t n = p.n_particles;
     P.L.values = ctx->values.get<double>(static_cast<size_t>(obs_count * n));
     CK(cudaEventRecord(ctx->ev[0], ctx->stream));
-    run_particles(ctx, P.L);
+    run_particles(ctx, P.L, &P);
     CK(cudaEventRecord(ctx->ev[1], ctx->stream));
     reduce_ad(ctx, P.L.values, n, obs_count, out);
     finish_stats(ctx);
@@ -621,7 +635,7 @@ smc_status smc_ad_shard_partials(smc_ctx* ctx, const smc_ad_problem* p, uint64_t
         const int64_t span = std::max<int64_t>(P.L.p_end - P.L.p_begin, 0);
         P.L.values = ctx->values.get<double>(static_cast<size_t>(std::max<int64_t>(p->n_obs * span, 1)));
         CK(cudaEventRecord(ctx->ev[0], ctx->stream));
-        run_particles(ctx, P.L);
+        run_particles(ctx, P.L, &P);
         CK(cudaEventRecord(ctx->ev[1], ctx->stream));
         const int64_t nloc = chunk_end - chunk_begin;
         if (nloc > 0) {
@@ -679,7 +693,7 @@ smc_status smc_ad_particle_values(smc_ctx* ctx, const smc_ad_problem* p, uint64_
         P.L.seed = seed;
         P.L.p_end = n;
         P.L.values = ctx->values.get<double>(static_cast<size_t>(n));
-        run_particles(ctx, P.L);
+        run_particles(ctx, P.L, &P);
         CK(cudaMemcpyAsync(out, P.L.values, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
     });

@@ -3,6 +3,8 @@
 // (host/scalarmc_forward_gpu.cpp) can rethrow the same std:: types.
 #include "host_problem.h"
 
+#include "disk_shape.h"
+
 #include <algorithm>
 #include <cmath>
 #include <limits>
@@ -245,6 +247,35 @@ void lattice_fill(const LatticeHost& s, const PreparedVelocity& v, double* dst) 
         const Slot g = gr.at(k1, 0);
         g0[2 * k1] = k1 * g.gr;
         g0[2 * k1 + 1] = k1 * g.gi;
+    }
+}
+
+void disk_fill(int K, const PreparedVelocity& v, double* dst) {
+    Grid gr = make_grid(v, true);
+    const int n_pairs = disk_n_pairs(K);
+    double* pairs = dst;
+    double* row0 = dst + 4 * n_pairs;
+    double* g0 = row0 + 2 * K;
+    int p = 0;
+    for (int k1 = 1; k1 <= K; ++k1) {
+        for (int j = 1; j <= disk_jmax(K, k1); ++j, ++p) {
+            const Slot gp = gr.at(k1, j), gm = gr.at(k1, -j);
+            double* c = pairs + 4 * p;
+            c[0] = gp.gr + gm.gr;  // alpha
+            c[1] = gp.gi + gm.gi;
+            c[2] = gp.gr - gm.gr;  // beta
+            c[3] = gp.gi - gm.gi;
+        }
+    }
+    for (int j = 1; j <= K; ++j) {
+        const Slot g = gr.at(0, j);
+        row0[2 * (j - 1)] = g.gr;
+        row0[2 * (j - 1) + 1] = g.gi;
+    }
+    for (int k1 = 1; k1 <= K; ++k1) {
+        const Slot g = gr.at(k1, 0);
+        g0[2 * (k1 - 1)] = g.gr;
+        g0[2 * (k1 - 1) + 1] = g.gi;
     }
 }
 

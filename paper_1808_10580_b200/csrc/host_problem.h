@@ -55,6 +55,9 @@ LatticeHost lattice_structure(const PreparedVelocity& v);
 // for the same mode set; writes stride() doubles at dst ([coef|row0|g0]).
 void lattice_fill(const LatticeHost& s, const PreparedVelocity& v, double* dst);
 
+// Coefficient block of the compile-time disk kernel (disk_shape.h layout).
+void disk_fill(int K, const PreparedVelocity& v, double* dst);
+
 // PriorSpec::modes (src/inference.cpp:24-40).
 std::vector<HostMode> prior_modes(int cutoff);
 

@@ -62,7 +62,8 @@ def test_device_normals_match_reference(ctx, golden):
         identical += int(np.sum(got.view(np.uint64) == want.view(np.uint64)))
         total += got.size
     assert worst < 1e-14
-    assert identical / total > 0.5  # libdevice vs glibc: equal except in the last ulp
+    # sincospi(2 u1) vs glibc sin/cos(2 pi u1): equal except in the last ulp
+    assert identical / total > 0.3
 
 
 # ---------------------------------------------------------------- AD -------
@@ -100,6 +101,21 @@ def test_c2_matches_reference(ctx, golden):
         assert np.max(np.abs(got - unhex(g["particles"][idx]))) < 1e-11
 
 
+def test_c2_lattice_kernel_matches_reference(ctx, golden, monkeypatch):
+    monkeypatch.setenv("SMC_DISABLE_DISK", "1")
+    g = golden["c2"]
+    spec = specs.c2_spec(unhex(g["u"]), n_particles=g["n_particles"])
+    assert_estimates(S.observe_ad(spec, 808, ctx=ctx), g["estimates"], 1.0)
+
+
+@pytest.mark.parametrize("ppt", ["1", "2"])
+def test_c2_disk_particles_per_thread(ctx, golden, monkeypatch, ppt):
+    monkeypatch.setenv("SMC_DISK_P", ppt)
+    g = golden["c2"]
+    spec = specs.c2_spec(unhex(g["u"]), n_particles=g["n_particles"])
+    assert_estimates(S.observe_ad(spec, 808, ctx=ctx), g["estimates"], 1.0)
+
+
 def test_c2_strict_matches_reference(ctx, golden):
     g = golden["c2"]
     spec = specs.c2_spec(unhex(g["u"]), n_particles=g["n_particles"], precision=S.Precision.fp64_strict)
@@ -135,7 +151,9 @@ def test_batched_equals_single_calls(ctx):
         spec.velocity = S.VelocityField.fourier(S.velocity_from_coefficients(prior, U[b]))
         single = S.observe_ad(spec, 99, ctx=ctx)
         for j, e in enumerate(single):
-            assert out[b, j]["mean"] == e.mean and out[b, j]["std_error"] == e.std_error
+            # batched runs the generic lattice kernel, single calls the disk kernel
+            assert abs(out[b, j]["mean"] - e.mean) <= 1e-13
+            assert abs(out[b, j]["std_error"] - e.std_error) <= 1e-12 * e.std_error
 
 
 def test_batched_per_sample_seeds(ctx):
