@@ -334,10 +334,11 @@ def _image_bytes(spec) -> int:
 
 def _ncu_traffic():
     """DRAM bytes per K1 launch from the committed ncu --set full capture."""
-    p = PROFILES / "k1_ncu_summary.json"
-    if p.exists():
+    caps = sorted(PROFILES.glob("r*_k1_c2.json"))
+    if caps:
         try:
-            return json.loads(p.read_text()).get("dram_bytes_per_launch")
+            d = json.loads(caps[-1].read_text())
+            return {"dram_bytes_per_launch": d.get("dram_bytes_per_launch"), "source": f"profiles/{caps[-1].name}"}
         except Exception:  # noqa: BLE001
             return None
     return None
