@@ -38,17 +38,31 @@ __device__ __forceinline__ void ad_particles_p(const AdLaunch& L, int obs, int s
     }
     const T dt = T(o.dt), dt_last = T(o.dt_last), sr = T(o.sr), sr_last = T(o.sr_last);
     const int64_t n = o.n_steps;
-    for (int64_t step = 0; step < n; ++step) {
-        T xi1[P], xi2[P], v1[P], v2[P];
+    // The noise of step s+1 does not depend on the path, so it is drawn one
+    // step ahead: its Philox/Box-Muller chain and step s's velocity series are
+    // independent instruction streams the scheduler interleaves (ILP that
+    // hides DFMA latency at modest occupancy).
+    T nx1[P], nx2[P];
+    auto draw = [&](int64_t step, T (&z1)[P], T (&z2)[P]) {
 #pragma unroll
         for (int p = 0; p < P; ++p) {
             const Uniform2 u = uniform_block(k0, k1, slot, particle[p], static_cast<uint64_t>(step));
             const T rad = sqrt(T(-2) * log_t(T(u.u0)));
             T sn, cs;
             sincospi_t(T(2) * T(u.u1), &sn, &cs);
-            xi1[p] = rad * cs;
-            xi2[p] = rad * sn;
+            z1[p] = rad * cs;
+            z2[p] = rad * sn;
         }
+    };
+    draw(0, nx1, nx2);
+    for (int64_t step = 0; step < n; ++step) {
+        T xi1[P], xi2[P], v1[P], v2[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            xi1[p] = nx1[p];
+            xi2[p] = nx2[p];
+        }
+        draw(step + 1, nx1, nx2);  // one block past the last step is drawn and discarded
         velocity(x1, x2, v1, v2);
         const bool last = step + 1 == n;
         const T h = last ? dt_last : dt;

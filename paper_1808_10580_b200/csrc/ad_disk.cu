@@ -242,12 +242,12 @@ cudaError_t dispatch_p(const AdLaunch& L, int K, const double* c, cudaStream_t s
     }
 }
 
-// Particles per thread: 2 for FP64 (each staged coefficient load feeds two
-// particles), overridable with SMC_DISK_P=1|2 for experiments.
+// Particles per thread: 1 by default; SMC_DISK_P=2 lets each staged
+// coefficient load feed two particles (more registers, fewer warps).
 template <class T>
 cudaError_t dispatch(const AdLaunch& L, int K, const double* c, cudaStream_t s) {
     const char* e = std::getenv("SMC_DISK_P");
-    const int P = (e && std::atoi(e) > 0) ? std::atoi(e) : 2;
+    const int P = (e && std::atoi(e) > 0) ? std::atoi(e) : 1;
     return P == 1 ? dispatch_p<T, 1>(L, K, c, s) : dispatch_p<T, 2>(L, K, c, s);
 }
 

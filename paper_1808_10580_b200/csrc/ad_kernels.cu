@@ -1,37 +1,52 @@
-// ad_kernels.cu — K1 with the generic lattice velocity (any K, any mode set,
-// per-sample coefficients for batched evaluation).  See ad_body.cuh for the
-// particle loop and velocity.cuh for the lattice series.  FP64 is the parity
-// path; FP32 is the optional fast mode (3-SE gate).
+// ad_kernels.cu — K1 with the generic tiled lattice velocity (any K, any mode
+// set, per-sample coefficient blocks for batched evaluation).  See
+// ad_body.cuh for the particle loop and velocity.cuh for the series.
+//
+// Each block serves one (sample, observation) and stages that sample's
+// coefficient block into shared memory once (converted to the compute type),
+// so every coefficient read in the step loop is a broadcast LDS.  Tables too
+// large to share an SM comfortably (> kSmemLimit) are read from global memory
+// through L1 instead (they fit L1 when shared memory is not carved out).
+// FP64 is the parity path; FP32 is the optional fast mode (3-SE gate).
 #include <cuda_runtime.h>
+
+#include <cstdlib>
 
 #include "ad_body.cuh"
 
 namespace smc {
-
 namespace {
 
 constexpr int kBlock = 256;
+constexpr size_t kSmemLimit = 64 * 1024;
 
-template <class T>
-__global__ void __launch_bounds__(kBlock) ad_particles(const AdLaunch L) {
+template <class T, bool SMEM>
+__global__ void __launch_bounds__(kBlock, 2) ad_particles(const AdLaunch L) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
     const int obs = blockIdx.y;
     const int sample = blockIdx.z;
+    const LatticeImg& lat = L.vel.lat;
+    const bool is_const = L.vel.is_constant;
+    const double* gblock = lat.coef + static_cast<int64_t>(sample) * lat.sample_stride;
+    T* sblock = reinterpret_cast<T*>(smem_raw);
+    if constexpr (SMEM) {
+        if (!is_const) {
+            for (int64_t i = threadIdx.x; i < lat.sample_stride; i += kBlock) sblock[i] = T(gblock[i]);
+            __syncthreads();
+        }
+    }
     const int64_t local = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x;
     const int64_t span = L.p_end - L.p_begin;
     if (local >= span) return;
-    const LatticeImg& lat = L.vel.lat;
-    const int64_t soff = static_cast<int64_t>(sample) * lat.sample_stride;
-    const double* coef = lat.coef + soff;
-    const double* row0 = lat.row0 + soff;
-    const double* g0 = lat.g0 + soff;
-    const bool is_const = L.vel.is_constant;
     const T c1 = T(L.vel.c1), c2 = T(L.vel.c2);
     ad_particle<T>(L, obs, sample, local, span, [&](T x1, T x2, T& v1, T& v2) {
         if (is_const) {
             v1 = c1;
             v2 = c2;
+        } else if constexpr (SMEM) {
+            velocity_lattice<T, T>(lat, sblock, x1, x2, v1, v2);
         } else {
-            velocity_lattice<T>(lat, coef, row0, g0, x1, x2, v1, v2);
+            velocity_lattice<T, double>(lat, gblock, x1, x2, v1, v2);
         }
     });
 }
@@ -42,7 +57,19 @@ cudaError_t launch(const AdLaunch& L, cudaStream_t s) {
     if (span <= 0) return cudaSuccess;
     const dim3 grid(static_cast<unsigned>((span + kBlock - 1) / kBlock), static_cast<unsigned>(L.n_obs),
                     static_cast<unsigned>(L.n_samples));
-    ad_particles<T><<<grid, kBlock, 0, s>>>(L);
+    const size_t smem = L.vel.is_constant ? 0 : static_cast<size_t>(L.vel.lat.sample_stride) * sizeof(T);
+    const bool use_smem = smem <= kSmemLimit && std::getenv("SMC_LATTICE_GLOBAL") == nullptr;
+    if (use_smem) {
+        static bool configured = false;
+        if (!configured) {
+            cudaFuncSetAttribute(ad_particles<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(kSmemLimit));
+            configured = true;
+        }
+        ad_particles<T, true><<<grid, kBlock, smem, s>>>(L);
+    } else {
+        ad_particles<T, false><<<grid, kBlock, 0, s>>>(L);
+    }
     return cudaGetLastError();
 }
 

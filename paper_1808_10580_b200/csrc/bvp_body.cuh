@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(kBvpBlock) bvp_walkers(const BvpLaunch L) {
                     v1 = T(L.vel.c1);
                     v2 = T(L.vel.c2);
                 } else {
-                    velocity_lattice<T>(lat, lat.coef, lat.row0, lat.g0, x1, x2, v1, v2);
+                    velocity_lattice<T, double>(lat, lat.coef, x1, x2, v1, v2);
                 }
             }
             T n1, n2;

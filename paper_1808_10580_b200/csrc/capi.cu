@@ -187,12 +187,11 @@ ScalarImg patch(const ScalarRef& r, unsigned char* base) {
 
 struct VelRef {
     VelImg img{};
-    size_t modes = 0, tile_rows = 0, tile_row = 0, coefs = 0;
-    int64_t n_coef = 0, n_row0 = 0;
+    size_t modes = 0, tiles = 0, coefs = 0;
 };
 
-// Velocity image: strict mode list + lattice structure + n_samples
-// coefficient sets (fills[i] for sample i).
+// Velocity image: strict mode list + tiled lattice structure + one
+// coefficient block per sample (fills[i] for sample i).
 VelRef add_velocity(Image& im, const PreparedVelocity& v, const std::vector<const PreparedVelocity*>& fills) {
     VelRef r;
     r.img.is_constant = v.is_constant ? 1 : 0;
@@ -209,21 +208,18 @@ VelRef add_velocity(Image& im, const PreparedVelocity& v, const std::vector<cons
     }
     r.modes = im.add_vec(modes);
     const LatticeHost L = lattice_structure(v);
-    r.tile_rows = im.add_vec(L.tile_rows);
-    r.tile_row = im.add_vec(L.tile_row);
-    const int64_t stride = L.stride();
-    r.coefs = im.reserve(static_cast<size_t>(stride) * fills.size() * sizeof(double));
+    r.tiles = im.add_vec(L.tiles);
+    r.coefs = im.reserve(static_cast<size_t>(L.stride) * fills.size() * sizeof(double));
     for (size_t b = 0; b < fills.size(); ++b)
-        lattice_fill(L, *fills[b], reinterpret_cast<double*>(im.bytes.data() + r.coefs) + b * stride);
+        lattice_fill(L, *fills[b], reinterpret_cast<double*>(im.bytes.data() + r.coefs) + b * L.stride);
     LatticeImg& li = r.img.lat;
-    li.sample_stride = stride;
+    li.sample_stride = L.stride;
     li.K = L.K;
     li.R = L.R;
-    li.J = L.J;
     li.J0 = L.J0;
     li.n_tiles = L.n_tiles;
-    r.n_coef = static_cast<int64_t>(L.coef.size());
-    r.n_row0 = static_cast<int64_t>(L.row0.size());
+    li.row0_off = static_cast<int32_t>(L.row0_off);
+    li.g0_off = static_cast<int32_t>(L.g0_off);
     return r;
 }
 
@@ -231,12 +227,8 @@ VelImg patch(const VelRef& r, unsigned char* base) {
     VelImg v = r.img;
     if (v.is_constant) return v;
     v.modes = reinterpret_cast<const ModeImg*>(base + r.modes);
-    v.lat.tile_rows = reinterpret_cast<const int32_t*>(base + r.tile_rows);
-    v.lat.tile_row = reinterpret_cast<const int2*>(base + r.tile_row);
-    const double* c = reinterpret_cast<const double*>(base + r.coefs);
-    v.lat.coef = c;
-    v.lat.row0 = c + r.n_coef;
-    v.lat.g0 = c + r.n_coef + r.n_row0;
+    v.lat.tiles = reinterpret_cast<const int2*>(base + r.tiles);
+    v.lat.coef = reinterpret_cast<const double*>(base + r.coefs);
     return v;
 }
 
@@ -599,12 +591,7 @@ smc_status smc_ad_observe_batched(smc_ctx* ctx, const smc_ad_problem* base, cons
             L.seed = seed;
             L.seeds = d_seeds ? d_seeds + b0 : nullptr;
             L.n_samples = static_cast<int32_t>(nb);
-            if (!L.vel.is_constant) {
-                const int64_t off = b0 * L.vel.lat.sample_stride;
-                L.vel.lat.coef += off;
-                L.vel.lat.row0 += off;
-                L.vel.lat.g0 += off;
-            }
+            if (!L.vel.is_constant) L.vel.lat.coef += b0 * L.vel.lat.sample_stride;
             L.values = values + b0 * n_obs * n;
             run_particles(ctx, L);
         }

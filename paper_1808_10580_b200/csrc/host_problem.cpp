@@ -138,10 +138,10 @@ void bvp_validate(const smc_bvp_problem& p) {
 // ---------------------------------------------------------------------------
 // Lattice packing.  For mode (k1,k2) with coefficient c, g = 2 c / |k|; the
 // velocity is v1 = sum -k2 Re(g E), v2 = sum k1 Re(g E), E = P1[k1] P2[k2].
-// A +/-j pair of row k1 with P2[j] = r + i s contributes, with
-// alpha = g+ + g-, beta = g+ - g-:
-//   A' += k1 (alpha r + i beta s)        (v2 = Re(P1 A'))
-//   B  += -j (beta r + i alpha s)        (v1 = Re(P1 B))
+// A +/-j pair of row k1 with P2[j] = r + i s and Q[j] = j P2[j] contributes,
+// with alpha = g+ + g-, beta = g+ - g-:
+//   A  += (alpha_re r - beta_im s) + i (alpha_im r + beta_re s)   v2 += k1 Re(P1 A)
+//   B' += (beta_re qr - alpha_im qs) + i (beta_im qr + alpha_re qs) v1 -= Re(P1 B')
 // ---------------------------------------------------------------------------
 namespace {
 
@@ -184,69 +184,54 @@ LatticeHost lattice_structure(const PreparedVelocity& v) {
     const Grid gr = make_grid(v, false);
     L.K = v.K;
     L.R = gr.R;
-    L.J = gr.J;
     L.J0 = gr.J0;
     const int jmax = std::max(gr.J, gr.J0);
     L.n_tiles = std::max(1, (jmax + kTileW - 1) / kTileW);
-    L.tile_rows.assign(static_cast<size_t>(L.n_tiles), 0);
-    L.tile_row.assign(static_cast<size_t>(L.n_tiles) * (L.R + 1), int2{0, 0});
-    int32_t off = 0;
+    int64_t off = 0;
     for (int t = 0; t < L.n_tiles; ++t) {
-        int last = (t == 0) ? L.R : 0;  // tile 0 folds every row's k2 = 0 term
-        for (int k1 = 1; k1 <= L.R; ++k1) {
-            const int cnt = std::clamp(gr.jrow[static_cast<size_t>(k1)] - kTileW * t, 0, kTileW);
-            L.tile_row[static_cast<size_t>(t) * (L.R + 1) + k1] = int2{off, cnt};
-            off += 8 * cnt;
-            if (cnt > 0) last = std::max(last, k1);
-        }
-        L.tile_rows[static_cast<size_t>(t)] = last;
+        int rows = (t == 0) ? L.R : 0;  // tile 0 folds every row's k2 = 0 term
+        for (int k1 = 1; k1 <= L.R; ++k1)
+            if (gr.jrow[static_cast<size_t>(k1)] > kTileW * t) rows = std::max(rows, k1);
+        L.tiles.push_back(int2{rows, static_cast<int>(off)});
+        off += static_cast<int64_t>(rows) * kTileW * 4;
     }
-    L.coef.assign(static_cast<size_t>(off), 0.0);
-    L.row0.assign(static_cast<size_t>(2 * L.J0), 0.0);
-    L.g0.assign(static_cast<size_t>(2 * (L.R + 1)), 0.0);
+    L.row0_off = off;
+    off += 2 * kTileW * L.n_tiles;
+    L.g0_off = off;
+    off += 2 * (L.R + 1);
+    L.stride = (off + 1) & ~int64_t(1);  // keep blocks 16-byte aligned
     return L;
 }
 
 void lattice_fill(const LatticeHost& s, const PreparedVelocity& v, double* dst) {
     Grid gr = make_grid(v, true);
-    double* coef = dst;
-    double* row0 = dst + s.coef.size();
-    double* g0 = row0 + s.row0.size();
-    std::fill(dst, dst + s.stride(), 0.0);
+    std::fill(dst, dst + s.stride, 0.0);
     for (int t = 0; t < s.n_tiles; ++t) {
-        for (int k1 = 1; k1 <= s.R; ++k1) {
-            const int2 tr = s.tile_row[static_cast<size_t>(t) * (s.R + 1) + k1];
-            for (int q = 0; q < tr.y; ++q) {
+        const int2 tl = s.tiles[static_cast<size_t>(t)];
+        for (int k1 = 1; k1 <= tl.x; ++k1) {
+            double* c = dst + tl.y + static_cast<int64_t>(k1 - 1) * kTileW * 4;
+            for (int q = 0; q < kTileW; ++q) {
                 const int j = kTileW * t + q + 1;
+                if (j > gr.K) break;
                 const Slot gp = gr.at(k1, j), gm = gr.at(k1, -j);
-                const double ar = gp.gr + gm.gr, ai = gp.gi + gm.gi;  // alpha
-                const double br = gp.gr - gm.gr, bi = gp.gi - gm.gi;  // beta
-                double* c = coef + tr.x + 8 * q;
-                // layout matches the kernel's double2 loads (ad_kernels.cu):
-                //   a0 = (c0, c1) -> Ar += c0 r + c1 s
-                //   a1 = (c2, c3) -> Ai += c2 r + c3 s
-                //   b0 = (c4, c5) -> Br += c4 r + c5 s
-                //   b1 = (c6, c7) -> Bi += c6 r + c7 s
-                c[0] = k1 * ar;
-                c[1] = -k1 * bi;
-                c[2] = k1 * ai;
-                c[3] = k1 * br;
-                c[4] = -j * br;
-                c[5] = j * ai;
-                c[6] = -j * bi;
-                c[7] = -j * ar;
+                c[4 * q + 0] = gp.gr + gm.gr;  // alpha
+                c[4 * q + 1] = gp.gi + gm.gi;
+                c[4 * q + 2] = gp.gr - gm.gr;  // beta
+                c[4 * q + 3] = gp.gi - gm.gi;
             }
         }
     }
+    double* row0 = dst + s.row0_off;
     for (int j = 1; j <= s.J0; ++j) {
         const Slot g = gr.at(0, j);
-        row0[2 * (j - 1)] = -j * g.gr;
-        row0[2 * (j - 1) + 1] = j * g.gi;
+        row0[2 * (j - 1)] = g.gr;
+        row0[2 * (j - 1) + 1] = g.gi;
     }
+    double* g0 = dst + s.g0_off;
     for (int k1 = 1; k1 <= s.R; ++k1) {
         const Slot g = gr.at(k1, 0);
-        g0[2 * k1] = k1 * g.gr;
-        g0[2 * k1 + 1] = k1 * g.gi;
+        g0[2 * k1] = g.gr;
+        g0[2 * k1 + 1] = g.gi;
     }
 }
 

@@ -41,18 +41,15 @@ double bvp_resolved_dt(const smc_bvp_problem& p, const PreparedVelocity& v);  //
 void bvp_validate(const smc_bvp_problem& p);         // forward_bvp.cpp:20-32
 bool domain_contains(const smc_domain& d, double x1, double x2);  // geometry.cpp:22-31
 
-// Lattice coefficients for one coefficient set.
+// Tiled lattice layout (images.h) for one mode set.
 struct LatticeHost {
-    int K = 0, R = 0, J = 0, J0 = 0, n_tiles = 1;
-    std::vector<int32_t> tile_rows;
-    std::vector<int2> tile_row;
-    std::vector<double> coef, row0, g0;
-    int64_t stride() const { return static_cast<int64_t>(coef.size() + row0.size() + g0.size()); }
+    int K = 0, R = 0, J0 = 0, n_tiles = 1;
+    std::vector<int2> tiles;      // (rows_t, offset)
+    int64_t row0_off = 0, g0_off = 0, stride = 0;
 };
 // Structure only (which (k1,k2) slots exist) from a mode list.
 LatticeHost lattice_structure(const PreparedVelocity& v);
-// Fill coefficient values for `v` into a structure built by lattice_structure
-// for the same mode set; writes stride() doubles at dst ([coef|row0|g0]).
+// Coefficients of `v` (same mode set as the structure): stride doubles at dst.
 void lattice_fill(const LatticeHost& s, const PreparedVelocity& v, double* dst);
 
 // Coefficient block of the compile-time disk kernel (disk_shape.h layout).

@@ -38,25 +38,25 @@ struct ModeImg {
     double re, im, d1, d2;
 };
 
-// Lattice coefficient image for the fast kernels.
-//   v2 = sum_{k1>=1} Re(P1[k1] * A(k1)),  v1 = Re(B(0)) + sum_{k1>=1} Re(P1[k1] * B(k1))
-//   A(k1) = k1 g_{k1,0} + sum_j [8-coefficient pair update with P2[j]]
-// Tiles cover j in [8t+1, 8t+8].  For tile t and row k1 in [1, rows[t]],
-// tile_row[t*(R+1)+k1] = (offset into coef, pair count n <= 8); the pair
-// coefficients are 8 doubles each.  Row 0 (k1 = 0) keeps 2 doubles per j.
+// Tiled lattice coefficients for the generic fast kernels.
+// Columns j are processed in tiles of 8 (j = 8t+1 .. 8t+8); tile t covers rows
+// k1 = 1..rows_t.  Per-sample block of doubles (sample_stride apart):
+//   [tile data][row0][g0]
+//   tile data: for t, for k1 = 1..rows_t: 8 pairs x (alpha_re, alpha_im,
+//              beta_re, beta_im), zero-padded past the row's last mode
+//   row0:      8 n_tiles x (g_re, g_im) of modes (0, j)
+//   g0:        (R+1) x (g_re, g_im) of modes (k1, 0)
+// with g = 2 c / |k|, alpha = g(k1,j) + g(k1,-j), beta = g(k1,j) - g(k1,-j).
 struct LatticeImg {
-    int64_t sample_stride;  // doubles between consecutive samples' coef/row0/g0 (batched)
-    int32_t K;        // max_wavenumber
-    int32_t R;        // largest k1 with any mode (rows 1..R)
-    int32_t J;        // largest |k2| with any mode
-    int32_t J0;       // largest j with a row-0 mode
-    int32_t n_tiles;  // ceil(J / 8)
-    int32_t pad_;
-    const int32_t* tile_rows;   // [n_tiles]: last row with pairs in tile t
-    const int2* tile_row;       // [n_tiles][R+1]: (offset, count)
-    const double* coef;         // pair coefficients
-    const double* row0;         // [J0][2]: (-j g_re, j g_im) for (0, j)
-    const double* g0;           // [R+1][2]: k1 * g_{k1,0}
+    int64_t sample_stride;  // doubles per sample block
+    int32_t K;
+    int32_t R;          // largest k1 with any mode
+    int32_t J0;         // largest j with a row-0 mode
+    int32_t n_tiles;
+    int32_t row0_off;   // offsets (doubles) inside a sample block
+    int32_t g0_off;
+    const int2* tiles;  // [n_tiles]: (rows_t, data offset in doubles)
+    const double* coef; // sample 0 block
 };
 
 struct VelImg {

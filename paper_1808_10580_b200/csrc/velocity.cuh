@@ -3,10 +3,11 @@
 // so it inherits that unit's contraction mode.
 //
 // velocity_lattice<T>: the fast form.  Rows of constant k1;
-// the +/-j pair of a row is one 8-FMA update against P2[j] = e^{2 pi i j x2}
-// held in registers (tiles of 8 j); each row folds into v through
-// P1[k1] = e^{2 pi i k1 x1}.  4 FMA per mode; all coefficient loads are
-// warp-uniform (one L1 broadcast per warp).
+// the +/-j pair of a row is one 8-FMA update on 4 coefficients against
+// P2[j] = e^{2 pi i j x2} and Q[j] = j P2[j] held in registers (tiles of 8 j);
+// each row folds into v through P1[k1] = e^{2 pi i k1 x1}.  4 FMA per mode;
+// all coefficient loads are warp-uniform broadcasts (shared memory when the
+// block can stage the table, else L1).
 //
 // velocity_strict<KCAP>: the reference's own loop — power tables by complex
 // recurrence, (k1,k2)-sorted mode loop, w = 2 Re(v e), v += w d.
@@ -22,79 +23,91 @@ constexpr int kLatticeTile = 8;
 __device__ __forceinline__ void sincospi_t(double a, double* s, double* c) { sincospi(a, s, c); }
 __device__ __forceinline__ void sincospi_t(float a, float* s, float* c) { sincospif(a, s, c); }
 
+// Four coefficients (alpha_re, alpha_im, beta_re, beta_im) of one pair.
 template <class T>
-__device__ __forceinline__ T ldc(const double* p) {
-    return static_cast<T>(__ldg(p));
+__device__ __forceinline__ void load4(const double* p, T& a, T& b, T& c, T& d) {
+    const double2 x = *reinterpret_cast<const double2*>(p);
+    const double2 y = *reinterpret_cast<const double2*>(p + 2);
+    a = T(x.x);
+    b = T(x.y);
+    c = T(y.x);
+    d = T(y.y);
+}
+template <class T>
+__device__ __forceinline__ void load4(const float* p, T& a, T& b, T& c, T& d) {
+    const float4 x = *reinterpret_cast<const float4*>(p);
+    a = T(x.x);
+    b = T(x.y);
+    c = T(x.z);
+    d = T(x.w);
+}
+template <class T, class CT>
+__device__ __forceinline__ void load2(const CT* p, T& a, T& b) {
+    a = T(p[0]);
+    b = T(p[1]);
 }
 
-template <class T>
-__device__ __forceinline__ void velocity_lattice(const LatticeImg& L, const double* __restrict__ coef,
-                                                 const double* __restrict__ row0, const double* __restrict__ g0,
-                                                 T x1, T x2, T& v1, T& v2) {
+// Generic tiled lattice evaluation (any K, any mode set).  `cf` points to one
+// sample's coefficient block (shared or global memory) in the images.h layout.
+template <class T, class CT>
+__device__ __forceinline__ void velocity_lattice(const LatticeImg& L, const CT* __restrict__ cf, T x1, T x2, T& v1,
+                                                 T& v2) {
     T s1, c1, s2, c2;
     sincospi_t(T(2) * x1, &s1, &c1);
     sincospi_t(T(2) * x2, &s2, &c2);
     T acc1 = T(0), acc2 = T(0);
-    T qr = T(1), qi = T(0);  // P2 at the end of the previous tile
-    const int R1 = L.R + 1;
+    T qr0 = T(1), qi0 = T(0);  // P2 at the end of the previous tile
     for (int t = 0; t < L.n_tiles; ++t) {
-        T r[kLatticeTile], s[kLatticeTile];
+        T pr[kLatticeTile], pi[kLatticeTile], qr[kLatticeTile], qi[kLatticeTile];
 #pragma unroll
         for (int q = 0; q < kLatticeTile; ++q) {
-            const T nr = fma(qr, c2, -qi * s2);
-            const T ni = fma(qr, s2, qi * c2);
-            qr = nr;
-            qi = ni;
-            r[q] = nr;
-            s[q] = ni;
+            const T nr = fma(qr0, c2, -qi0 * s2);
+            const T ni = fma(qr0, s2, qi0 * c2);
+            qr0 = nr;
+            qi0 = ni;
+            pr[q] = nr;
+            pi[q] = ni;
+            const T j = T(kLatticeTile * t + q + 1);
+            qr[q] = j * nr;
+            qi[q] = j * ni;
         }
-        // Row k1 = 0: modes (0, j); P1 = 1 and only Re(B) feeds v1.
-        const int j0 = kLatticeTile * t;
-        const int n0 = min(kLatticeTile, L.J0 - j0);
-        if (n0 > 0) {
-            const double2* w = reinterpret_cast<const double2*>(row0) + j0;
+        // Row k1 = 0: modes (0, j), P1 = 1:  v1 -= sum (g_re qr - g_im qs)
+        if (kLatticeTile * t < L.J0) {
+            const CT* w = cf + L.row0_off + 2 * kLatticeTile * t;
 #pragma unroll
             for (int q = 0; q < kLatticeTile; ++q) {
-                if (q < n0) {
-                    const double2 c = __ldg(w + q);
-                    acc1 = fma(T(c.x), r[q], acc1);
-                    acc1 = fma(T(c.y), s[q], acc1);
-                }
+                T gr, gi;
+                load2(w + 2 * q, gr, gi);
+                acc1 = fma(gr, -qr[q], acc1);
+                acc1 = fma(gi, qi[q], acc1);
             }
         }
-        T p1r = T(1), p1i = T(0);
-        const int rows = __ldg(L.tile_rows + t);
-        for (int k1 = 1; k1 <= rows; ++k1) {
-            const T nr = fma(p1r, c1, -p1i * s1);
-            p1i = fma(p1r, s1, p1i * c1);
-            p1r = nr;
-            const int2 tr = __ldg(L.tile_row + t * R1 + k1);
+        const int2 tl = L.tiles[t];
+        T p1r = c1, p1i = s1;
+        const CT* c = cf + tl.y;
+        for (int k1 = 1; k1 <= tl.x; ++k1, c += 4 * kLatticeTile) {
+            if (k1 > 1) {
+                const T nr = fma(p1r, c1, -p1i * s1);
+                p1i = fma(p1r, s1, p1i * c1);
+                p1r = nr;
+            }
             T Ar = T(0), Ai = T(0), Br = T(0), Bi = T(0);
-            if (t == 0) {
-                const double2 g = __ldg(reinterpret_cast<const double2*>(g0) + k1);
-                Ar = T(g.x);
-                Ai = T(g.y);
-            }
-            const double2* c = reinterpret_cast<const double2*>(coef + tr.x);
+            if (t == 0) load2(cf + L.g0_off + 2 * k1, Ar, Ai);
 #pragma unroll
             for (int q = 0; q < kLatticeTile; ++q) {
-                if (q < tr.y) {
-                    const double2 a0 = __ldg(c + 4 * q + 0);
-                    const double2 a1 = __ldg(c + 4 * q + 1);
-                    const double2 b0 = __ldg(c + 4 * q + 2);
-                    const double2 b1 = __ldg(c + 4 * q + 3);
-                    Ar = fma(T(a0.x), r[q], Ar);
-                    Ai = fma(T(a1.x), r[q], Ai);
-                    Br = fma(T(b0.x), r[q], Br);
-                    Bi = fma(T(b1.x), r[q], Bi);
-                    Ar = fma(T(a0.y), s[q], Ar);
-                    Ai = fma(T(a1.y), s[q], Ai);
-                    Br = fma(T(b0.y), s[q], Br);
-                    Bi = fma(T(b1.y), s[q], Bi);
-                }
+                T ar, ai, br, bi;
+                load4(c + 4 * q, ar, ai, br, bi);
+                Ar = fma(ar, pr[q], Ar);
+                Ai = fma(ai, pr[q], Ai);
+                Br = fma(br, qr[q], Br);
+                Bi = fma(bi, qr[q], Bi);
+                Ar = fma(bi, -pi[q], Ar);
+                Ai = fma(br, pi[q], Ai);
+                Br = fma(ai, -qi[q], Br);
+                Bi = fma(ar, qi[q], Bi);
             }
-            acc2 = fma(p1r, Ar, fma(-p1i, Ai, acc2));
-            acc1 = fma(p1r, Br, fma(-p1i, Bi, acc1));
+            acc2 = fma(T(k1), fma(p1r, Ar, -p1i * Ai), acc2);
+            acc1 = fma(-p1r, Br, fma(p1i, Bi, acc1));
         }
     }
     v1 = acc1;

@@ -17,6 +17,8 @@ ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--particles", type=int, default=0)
 ap.add_argument("--lattice", action="store_true", help="disable the compile-time disk kernel")
 ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32", "fp64_strict"])
+ap.add_argument("--cutoff", type=int, default=0, help="C2 shape with a K=cutoff prior-draw velocity (0: as config)")
+ap.add_argument("--constant-velocity", action="store_true", help="C2 shape with v = (0.3, -0.2)")
 args = ap.parse_args()
 if args.lattice:
     os.environ["SMC_DISABLE_DISK"] = "1"
@@ -25,13 +27,38 @@ import bench  # noqa: E402
 import paper_1808_10580_b200 as S  # noqa: E402
 
 ctx = S.default_context(0)
+if args.config == "c4":
+    # B pCN proposals u_b = sqrt(1-beta^2) u0 + beta xi_b, K=25 prior, CRN seed 808
+    import math
+    import numpy as np
+    import specs
+    B = args.particles or 4096
+    prior = specs.C4_PRIOR
+    u0 = S.prior_draw(prior, 808, 0xBE9C4, 1, ctx)
+    stds = prior.component_stds()
+    xi = np.random.default_rng(0).normal(size=(B, prior.dimension())) * stds
+    U = math.sqrt(1 - 0.02 ** 2) * u0[None, :] + 0.02 * xi
+    base = specs.c4_base(n_particles=1024, precision=S.Precision[args.precision])
+    for _ in range(args.reps):
+        out = S.observe_ad_batched(base, prior, U, 808, ctx=ctx)
+    st = ctx.stats()
+    print(f"c4 B={B}: kernel {st.particle_kernel_ms:.3f} ms reduce {st.reduce_ms:.3f} ms steps {st.particle_steps} -> "
+          f"{st.particle_steps / st.particle_kernel_ms * 1e3:.4g} particle-steps/s; "
+          f"{14 * 980 + 12 * 24 + 20} flop/step -> {(14 * 980 + 12 * 24 + 20) * st.particle_steps / st.particle_kernel_ms / 1e9:.2f} TFLOP/s")
+    sys.exit(0)
 spec, steps, F, desc = bench.build_workload(args.config, ctx)
+if args.cutoff:
+    import specs
+    prior = S.PriorSpec(args.cutoff, 1.0, 2.5)
+    spec.velocity = S.VelocityField.fourier(S.velocity_from_coefficients(prior, S.prior_draw(prior, 808, 0xBE9C4, 0, ctx)))
+if args.constant_velocity:
+    spec.velocity = S.VelocityField.constant((0.3, -0.2))
 if args.particles:
     spec.n_particles = args.particles
 spec.precision = S.Precision[args.precision]
 for _ in range(args.reps):
     est = S.observe_ad(spec, 808, ctx=ctx)
 st = ctx.stats()
-print(f"{args.config}: kernel {st.particle_kernel_ms:.3f} ms reduce {st.reduce_ms:.3f} ms "
+print(f"{args.config} K={args.cutoff} const={args.constant_velocity} P={os.environ.get('SMC_DISK_P', '-')}: kernel {st.particle_kernel_ms:.3f} ms reduce {st.reduce_ms:.3f} ms "
       f"steps {st.particle_steps} -> {st.particle_steps / st.particle_kernel_ms * 1e3:.4g} particle-steps/s; "
       f"mean[0]={est[0].mean:.15g}")

@@ -1,0 +1,186 @@
+// ubench_dfma.cu — FP64 pipe microbenchmarks on B200 (sm_100a): what limits a
+// DFMA-dense kernel?  Variants:
+//   uniform : a[q] = fma(a[q], b, c), b/c warp-uniform (the peak recipe)
+//   regs3   : a[q] = fma(x[q], y[q], a[q]), three distinct register operands
+//   pairs   : the K1 lattice pair update: 4 accumulators, coefficients from
+//             shared memory (LDS.128 broadcast), powers in registers
+// each at several warps per SM.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o ubench_dfma tools/ubench_dfma.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+template <int CH>
+__global__ void k_uniform(int iters, double b, double c, double* sink) {
+    double a[CH];
+#pragma unroll
+    for (int q = 0; q < CH; ++q) a[q] = 1.0 + 1e-9 * (threadIdx.x + q);
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+        for (int q = 0; q < CH; ++q) a[q] = fma(a[q], b, c);
+    double s = 0;
+#pragma unroll
+    for (int q = 0; q < CH; ++q) s += a[q];
+    if (s == 12345.0) sink[blockIdx.x] = s;
+}
+
+template <int CH>
+__global__ void k_regs3(int iters, double* sink) {
+    double a[CH], x[CH], y[CH];
+#pragma unroll
+    for (int q = 0; q < CH; ++q) {
+        a[q] = 1.0 + 1e-9 * (threadIdx.x + q);
+        x[q] = 0.999999 + 1e-12 * q * threadIdx.x;
+        y[q] = 1e-12 * (q + 1);
+    }
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+        for (int q = 0; q < CH; ++q) a[q] = fma(a[q], x[q], y[(q + 1) % CH]);
+    double s = 0;
+#pragma unroll
+    for (int q = 0; q < CH; ++q) s += a[q];
+    if (s == 12345.0) sink[blockIdx.x] = s;
+}
+
+// K1-like: J powers in registers, 4 accumulators per row, 4 coefs per pair from smem
+template <int J>
+__global__ void k_pairs(int iters, const double* coef_g, double* sink) {
+    __shared__ __align__(16) double coef[4 * J * 8];
+    for (int i = threadIdx.x; i < 4 * J * 8; i += blockDim.x) coef[i] = coef_g[i];
+    __syncthreads();
+    const unsigned base = static_cast<unsigned>(__cvta_generic_to_shared(coef));
+    double pr[J], pi[J], qr[J], qi[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+        pr[j] = 0.5 + 1e-3 * j + 1e-9 * threadIdx.x;
+        pi[j] = 0.25 - 1e-3 * j;
+        qr[j] = (j + 1) * pr[j];
+        qi[j] = (j + 1) * pi[j];
+    }
+    double acc1 = 0, acc2 = 0;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int row = 0; row < 8; ++row) {
+            double Ar = 0, Ai = 0, Br = 0, Bi = 0;
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                double ar, ai, br, bi;
+                asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(ar), "=d"(ai) : "r"(base + 32 * (row * J + j)));
+                asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(br), "=d"(bi) : "r"(base + 32 * (row * J + j) + 16));
+                Ar = fma(ar, pr[j], Ar);
+                Ai = fma(ai, pr[j], Ai);
+                Br = fma(br, qr[j], Br);
+                Bi = fma(bi, qr[j], Bi);
+                Ar = fma(bi, -pi[j], Ar);
+                Ai = fma(br, pi[j], Ai);
+                Br = fma(ai, -qi[j], Br);
+                Bi = fma(ar, qi[j], Bi);
+            }
+            acc2 = fma(Ar, 0.3, fma(Ai, -0.2, acc2));
+            acc1 = fma(Br, 0.7, fma(Bi, 0.1, acc1));
+        }
+#pragma unroll
+        for (int j = 0; j < J; ++j) pr[j] = fma(pr[j], 1e-17, acc1 * 1e-300);
+    }
+    if (acc1 + acc2 == 12345.0) sink[blockIdx.x] = acc1;
+}
+
+// two particles share each shared-memory coefficient load
+template <int J>
+__global__ void k_pairs2(int iters, const double* coef_g, double* sink) {
+    __shared__ __align__(16) double coef[4 * J * 8];
+    for (int i = threadIdx.x; i < 4 * J * 8; i += blockDim.x) coef[i] = coef_g[i];
+    __syncthreads();
+    const unsigned base = static_cast<unsigned>(__cvta_generic_to_shared(coef));
+    double pr[2][J], pi[2][J], qr[2][J], qi[2][J];
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+        pr[p][j] = 0.5 + 1e-3 * j + 1e-9 * threadIdx.x + p;
+        pi[p][j] = 0.25 - 1e-3 * j;
+        qr[p][j] = (j + 1) * pr[p][j];
+        qi[p][j] = (j + 1) * pi[p][j];
+    }
+    double acc1[2] = {0, 0}, acc2[2] = {0, 0};
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int row = 0; row < 8; ++row) {
+            double Ar[2] = {0, 0}, Ai[2] = {0, 0}, Br[2] = {0, 0}, Bi[2] = {0, 0};
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                double ar, ai, br, bi;
+                asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(ar), "=d"(ai) : "r"(base + 32 * (row * J + j)));
+                asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(br), "=d"(bi) : "r"(base + 32 * (row * J + j) + 16));
+#pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    Ar[p] = fma(ar, pr[p][j], Ar[p]);
+                    Ai[p] = fma(ai, pr[p][j], Ai[p]);
+                    Br[p] = fma(br, qr[p][j], Br[p]);
+                    Bi[p] = fma(bi, qr[p][j], Bi[p]);
+                    Ar[p] = fma(bi, -pi[p][j], Ar[p]);
+                    Ai[p] = fma(br, pi[p][j], Ai[p]);
+                    Br[p] = fma(ai, -qi[p][j], Br[p]);
+                    Bi[p] = fma(ar, qi[p][j], Bi[p]);
+                }
+            }
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                acc2[p] = fma(Ar[p], 0.3, fma(Ai[p], -0.2, acc2[p]));
+                acc1[p] = fma(Br[p], 0.7, fma(Bi[p], 0.1, acc1[p]));
+            }
+        }
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int j = 0; j < J; ++j) pr[p][j] = fma(pr[p][j], 1e-17, acc1[p] * 1e-300);
+    }
+    if (acc1[0] + acc2[1] == 12345.0) sink[blockIdx.x] = acc1[0];
+}
+
+template <class F>
+double time_kernel(F launch) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    launch();
+    cudaEventRecord(a);
+    launch();
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms;
+}
+
+int main() {
+    int sms;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    double* sink;
+    cudaMalloc(&sink, 1 << 20);
+    double* coef;
+    cudaMalloc(&coef, 8 * 4096);
+    cudaMemset(coef, 0, 8 * 4096);
+    const int iters = 20000;
+    for (int warps : {4, 8, 16, 32, 64}) {
+        const int threads = 128, blocks = sms * warps * 32 / threads;
+        double ms = time_kernel([&] { k_uniform<8><<<blocks, threads>>>(iters, 0.999999999, 1e-12, sink); });
+        double fl = 2.0 * 8 * iters * double(blocks) * threads;
+        printf("uniform ch8  warps/SM=%2d  %.2f TFLOP/s\n", warps, fl / ms / 1e9);
+        ms = time_kernel([&] { k_uniform<4><<<blocks, threads>>>(iters, 0.999999999, 1e-12, sink); });
+        fl = 2.0 * 4 * iters * double(blocks) * threads;
+        printf("uniform ch4  warps/SM=%2d  %.2f TFLOP/s\n", warps, fl / ms / 1e9);
+        ms = time_kernel([&] { k_regs3<8><<<blocks, threads>>>(iters, sink); });
+        fl = 2.0 * 8 * iters * double(blocks) * threads;
+        printf("regs3 ch8    warps/SM=%2d  %.2f TFLOP/s\n", warps, fl / ms / 1e9);
+        ms = time_kernel([&] { k_pairs<7><<<blocks, threads>>>(iters / 20, coef, sink); });
+        fl = 2.0 * (8 * (8 * 7 + 4) + 7) * (iters / 20) * double(blocks) * threads;
+        printf("pairs J=7    warps/SM=%2d  %.2f TFLOP/s\n", warps, fl / ms / 1e9);
+        if (warps <= 32) {
+            ms = time_kernel([&] { k_pairs2<7><<<blocks, threads>>>(iters / 20, coef, sink); });
+            printf("pairs2 (P=2) warps/SM=%2d  %.2f TFLOP/s\n", warps, 2 * fl / ms / 1e9);
+        }
+    }
+    cudaError_t e = cudaGetLastError();
+    printf("status %s\n", cudaGetErrorString(e));
+    return 0;
+}
