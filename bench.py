@@ -59,44 +59,85 @@ def flops_ad(K: int, M: int) -> int:
     return 14 * M + 12 * (K - 1) + 20
 
 
-def build_workload(name: str, ctx):
+def flops_bvp(n_bumps: int, K: int = 0, M: int = 0) -> int:
+    """F_BVP = 10 + 4 + 4 + 8 N_bump + 2 (+ F_velocity)."""
+    return 10 + 4 + 4 + 8 * n_bumps + 2 + (14 * M + 12 * (K - 1) if M else 0)
+
+
+def c5_spec(S, u):
+    """K=80 (M=10040), kappa 3e-5, theta_0 = 100-term
+    cosine series (|k| <= 8, random amplitudes), 64 observations
+    (j/8, j/8) x t in {1/16 .. 8/16}, dt 5e-4, 32768 particles/obs."""
+    prior = S.PriorSpec(80, 1.0, 2.5)
+    rng = np.random.default_rng(5)
+    terms = []
+    for k1 in range(-8, 9):
+        for k2 in range(-8, 9):
+            if len(terms) < 100 and 0 < k1 * k1 + k2 * k2 <= 64:
+                terms.append((float(rng.normal()) / (k1 * k1 + k2 * k2), (2 * math.pi * k1, 2 * math.pi * k2),
+                              float(rng.random() * 2 * math.pi)))
+    obs = [S.AdObservation(t / 16.0, S.Vec2(j / 8.0, j / 8.0)) for j in range(8) for t in range(1, 9)]
+    return S.AdProblemSpec(velocity=S.VelocityField.fourier(S.velocity_from_coefficients(prior, u)),
+                           diffusion=S.DiffusionModel.isotropic(3e-5),
+                           initial_condition=S.ScalarField.cosine_series(terms), observations=obs, dt=5e-4,
+                           n_particles=32768)
+
+
+def build_workload(name: str, ctx, u_source=None):
+    """-> (kind, payload, particle-steps per evaluation (None: counted on
+    device), flops per particle-step, description).  u_source(prior, seed,
+    obs, particle) draws prior coefficients (device normals on our arm, the
+    reference's prior_draw on the reference arm)."""
     import paper_1808_10580_b200 as S
     import specs
+    draw = u_source or (lambda prior, seed, obs, particle: S.prior_draw(prior, seed, obs, particle, ctx))
     if name == "c2":
-        u = S.prior_draw(specs.C2_PRIOR, 808, 0xBE9C4, 0, ctx)  # benchmark.cpp:69-71 recipe
+        u = draw(specs.C2_PRIOR, 808, 0xBE9C4, 0)  # benchmark.cpp:69-71 recipe
         spec = specs.c2_spec(u, n_particles=100_000)
         K, M = 8, len(specs.C2_PRIOR.modes())
         desc = {"workload": "C2: AD forward map, K=8 Fourier velocity (M=98, N_u=197), 9 obs, 1e5 particles/obs, "
                             "1000 EM steps, FP64", "K": K, "modes": M, "n_obs": 9, "particles_per_obs": 100_000,
                 "em_steps": 1000, "seed": 808}
+        kind, payload, F = "ad", spec, flops_ad(K, M)
     elif name == "c1":
         spec = specs.c1_two_mode(n_particles=10_000)
-        K, M = 1, 2
-        desc = {"workload": "C1: shipped forward_ad_two_mode.json (K=1, M=2, 3 obs, 1e4 particles)", "K": K,
-                "modes": M, "n_obs": 3, "particles_per_obs": 10_000, "seed": 7}
+        desc = {"workload": "C1: shipped forward_ad_two_mode.json (K=1, M=2, 3 obs, 1e4 particles)", "K": 1,
+                "modes": 2, "n_obs": 3, "particles_per_obs": 10_000, "seed": 7}
+        kind, payload, F = "ad", spec, flops_ad(1, 2)
     elif name == "c5":
-        prior = S.PriorSpec(80, 1.0, 2.5)
-        u = S.prior_draw(prior, 808, 0xBE9C4, 2, ctx)
-        rng = np.random.default_rng(5)
-        terms = []
-        for k1 in range(-8, 9):
-            for k2 in range(-8, 9):
-                if len(terms) < 100 and 0 < k1 * k1 + k2 * k2 <= 64:
-                    terms.append((float(rng.normal()) / (k1 * k1 + k2 * k2), (2 * math.pi * k1, 2 * math.pi * k2),
-                                  float(rng.random() * 2 * math.pi)))
-        obs = [S.AdObservation(t / 16.0, S.Vec2(j / 8.0, j / 8.0)) for j in range(8) for t in range(1, 9)]
-        spec = S.AdProblemSpec(velocity=S.VelocityField.fourier(S.velocity_from_coefficients(prior, u)),
-                               diffusion=S.DiffusionModel.isotropic(3e-5),
-                               initial_condition=S.ScalarField.cosine_series(terms), observations=obs, dt=5e-4,
-                               n_particles=32768)
-        K, M = 80, len(prior.modes())
-        desc = {"workload": "C5: AD forward map, K=80 (M=10040), 64 obs, 32768 particles/obs, FP64", "K": K,
-                "modes": M, "n_obs": 64, "particles_per_obs": 32768, "seed": 808}
+        u = draw(S.PriorSpec(80, 1.0, 2.5), 808, 0xBE9C4, 2)
+        spec = c5_spec(S, u)
+        desc = {"workload": "C5: AD forward map, K=80 (M=10040, N_u=20081), 64 obs, 32768 particles/obs, FP64",
+                "K": 80, "modes": 10040, "n_obs": 64, "particles_per_obs": 32768, "seed": 808}
+        kind, payload, F = "ad", spec, flops_ad(80, 10040)
+    elif name == "c3":
+        spec = specs.c3_spec(n_particles=1_000_000)
+        desc = {"workload": "C3: Dirichlet BVP, box, v=(1,1), kappa 0.282, 3 bumps F=(1,-0.5,2), 25 obs, "
+                            "1e6 walkers/obs, dt 1.5e-4, FP64", "n_obs": 25, "walkers_per_obs": 1_000_000,
+                "seed": 606}
+        kind, payload, F = "bvp", spec, flops_bvp(3)
+    elif name == "c4":
+        prior = specs.C4_PRIOR
+        u0 = draw(prior, 808, 0xBE9C4, 1)
+        B = 4096
+        # pCN proposals u_b = sqrt(1-beta^2) u0 + beta xi_b, xi_b ~ prior (inference.cpp:141-144)
+        U = np.stack([math.sqrt(1 - 0.02 ** 2) * u0 + 0.02 * draw(prior, 4242, 0xFFFFFFFF, b) for b in range(B)])
+        base = specs.c4_base(n_particles=1024)
+        desc = {"workload": "C4: batched MCMC, 4096 pCN proposals per launch, K=25 (M=980) velocity, 9 obs, "
+                            "1024 particles/obs, CRN seed 808, FP64", "K": 25, "modes": 980, "samples": B,
+                "n_obs": 9, "particles_per_obs": 1024, "seed": 808}
+        kind, payload, F = "batched", (base, prior, U), flops_ad(25, 980)
     else:
         raise SystemExit(f"unknown config {name}")
-    dt = spec.resolved_dt()
-    steps = sum(int(math.ceil(o.t / dt)) for o in spec.observations) * spec.n_particles
-    return spec, steps, flops_ad(K, M), desc
+    if kind == "ad":
+        dt = payload.resolved_dt()
+        steps = sum(int(math.ceil(o.t / dt)) for o in payload.observations) * payload.n_particles
+    elif kind == "batched":
+        base, prior, U = payload
+        steps = sum(int(math.ceil(o.t / base.resolved_dt())) for o in base.observations) * base.n_particles * len(U)
+    else:
+        steps = None  # exit times are random: counted on device
+    return kind, payload, steps, F, desc
 
 
 # ---------------------------------------------------------------------------
@@ -156,29 +197,75 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU baseline: the reference compiled from its own sources (oracle/_ref)
 # ---------------------------------------------------------------------------
-def cpu_reference_sample(spec, steps_per_eval: int, budget_s: float = 20.0):
-    """Time the reference observe_ad (workers = all host cores) on a bounded
-    sample of the workload: same spec, fewer particles per observation.
-    1 warm-up + median of 3 (benchmark.cpp:39-52 methodology)."""
+def reference_runner(config: str, R, cores: int, budget_s: float):
+    """A bounded sample of `config` on the reference (oracle/_ref, the
+    reference compiled from its own sources) with workers = cores:
+    -> (particle-steps per run, run(), description).  Inputs follow the same
+    recipes as our arm, drawn with the reference's own prior_draw.  The
+    reference's executor parallelises one observation over 1024-particle
+    chunks (executor.cpp:45-85), so samples keep >= 1024 x cores particles per
+    observation where the full config has them."""
     import copy
+    kind, payload, steps, F, desc = build_workload(
+        config, None, u_source=lambda prior, seed, obs, particle: R.prior_draw(prior, seed, obs, particle))
+    rate = 3.0e9 / F * cores  # ~3 Gflop/s/core on the reference's mode loop (SURVEY.md §6)
+    if kind == "ad" and config != "c5":
+        spec = payload
+        per_particle = steps / spec.n_particles
+        n = int(max(1024 * cores, budget_s * rate / per_particle))
+        n = min(spec.n_particles, n)
+        sample = copy.copy(spec)
+        sample.n_particles = n
+        return per_particle * n, lambda: R.observe_ad(sample, 808, cores), \
+            f"observe_ad, all {len(spec.observations)} obs, {n} particles/obs (of {spec.n_particles}), " \
+            f"workers={cores}"
+    if kind in ("ad", "batched"):
+        # one observation (the shortest time) of the evaluation, 1024 x cores particles
+        if kind == "ad":
+            spec = copy.copy(payload)
+            u = None
+        else:
+            base, prior, U = payload
+            spec = copy.copy(base)
+            u = U[0]
+        j = int(np.argmin([o.t for o in spec.observations]))
+        spec.observations = [spec.observations[j]]
+        spec.n_particles = 1024 * cores
+        per = int(math.ceil(spec.observations[0].t / spec.resolved_dt())) * spec.n_particles
+        if u is None:
+            run = lambda: R.observe_ad(spec, 808, cores)  # noqa: E731
+        else:
+            run = lambda: R.observe_ad_u(spec, prior, u, 808, cores)  # noqa: E731
+        return per, run, f"observe_ad on observation {j} only (t={spec.observations[0].t:g}), " \
+                         f"{spec.n_particles} particles, workers={cores}" + \
+                         (", proposal 0 of the batch" if u is not None else "")
+    # bvp: walker-steps of the sample from the reference's own simulate_to_exit
+    spec = payload
+    sample = copy.copy(spec)
+    n = int(max(64, min(spec.n_particles, 1024 * cores)))
+    sample.n_particles = n
+    probe = 32
+    mean_steps = float(np.mean([R.bvp_particle_values(spec, j, 606, probe)[3].mean()
+                                for j in range(len(spec.observations))]))
+    return mean_steps * n * len(spec.observations), lambda: R.observe_bvp(sample, 606, cores), \
+        f"observe_bvp with {n} walkers/obs (of {spec.n_particles}), workers={cores}; walker-steps from " \
+        f"{probe} walkers/obs via the reference's simulate_to_exit"
+
+
+def cpu_reference_sample(config: str, ctx, per_eval: float, budget_s: float = 6.0):
+    """cpu_baseline: 1 warm-up + median of 3 bounded runs
+    (benchmark.cpp:39-52 methodology) on all host cores."""
     from oracle.oracle import Reference
     R = Reference()
     cores = os.cpu_count() or 1
-    sample = copy.copy(spec)
-    per_particle = steps_per_eval / spec.n_particles
-    # size so one run is ~budget/5 s at ~1.5e6 particle-steps/s/core (K=8 rate)
-    n = int(max(64, min(spec.n_particles, (budget_s / 5.0) * 1.5e6 * cores / per_particle)))
-    sample.n_particles = n
-    sample.precision = spec.precision
-    R.observe_ad(sample, 808, cores)  # warm-up
+    steps, run, sample = reference_runner(config, R, cores, budget_s)
+    run()
     times = []
     for _ in range(3):
         t0 = time.perf_counter()
-        R.observe_ad(sample, 808, cores)
+        run()
         times.append(time.perf_counter() - t0)
-    t = statistics.median(times)
-    return (per_particle * n) / t, cores, f"observe_ad with {n} particles/obs (of {spec.n_particles}), " \
-                                          f"median of 3 after 1 warm-up, workers={cores}"
+    return steps / statistics.median(times), cores, sample + ", median of 3 after 1 warm-up"
 
 
 # ---------------------------------------------------------------------------
@@ -193,46 +280,101 @@ def run_ours(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) if args.device < 0 else args.device
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:  # multi-rank plumbing test on fewer GPUs (host-staged all-gathers)
+            dist.init_process_group("gloo")
+    red_dev = "cuda" if args.dist_backend == "nccl" else "cpu"
     ctx = S.default_context(local)
     stream = torch.cuda.Stream(device=local)
     torch.cuda.set_stream(stream)
     S.load_library().smc_set_stream(ctx.handle, stream.cuda_stream)
 
-    spec, steps_per_eval, F, desc = build_workload(args.config, ctx)
+    kind, payload, steps_per_eval, F, desc = build_workload(args.config, ctx)
     peak = ctx.fp64_peak_tflops(300.0)
-
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
 
-    def device_step():
-        """One evaluation through the device-level (sharded) path: inputs
-        resident, returns (kernel_ms, launches)."""
-        ops = D.DeviceOps(spec, 808, ctx)
+    def timed(fn):
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        before = ctx.stats().total_launches
+        t0.record(stream)
+        k_ms, steps = fn()
+        t1.record(stream)
+        t1.synchronize()
+        return t0.elapsed_time(t1), k_ms, ctx.stats().total_launches - before, steps
+
+    if kind == "ad":
+        spec = payload
         n_chunks = D.num_chunks(spec.n_particles)
         b, e = D.chunk_range(n_chunks, rank, world)
         counts = [D.chunk_range(n_chunks, r, world)[1] - D.chunk_range(n_chunks, r, world)[0] for r in range(world)]
-        before = ctx.stats().total_launches
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
-        t0.record(stream)
-        parts = ops.partials(b, e)
-        k_ms = ctx.stats().particle_kernel_ms
-        full = ops.all_gather(parts, counts)
-        sums = ops.finish(full)
-        means = ops.divide(sums, spec.n_particles)
-        fullsq = ops.all_gather(ops.sq_partials(means, b, e), counts)
-        ops.finish(fullsq)
-        t1.record(stream)
-        t1.synchronize()
-        return t0.elapsed_time(t1), k_ms, ctx.stats().total_launches - before
+        my_steps = steps_per_eval * (e - b) / n_chunks  # chunk-proportional (last chunk may be partial)
 
-    def e2e_step():
-        if world == 1:
-            return S.observe_ad(spec, 808, ctx=ctx)
-        return D.observe_ad_sharded(spec, 808, rank, world, ctx)
+        def device_step():
+            """One evaluation through the device-level sharded path, inputs resident."""
+            ops = D.DeviceOps(spec, 808, ctx)
+
+            def run():
+                parts = ops.partials(b, e)
+                k = ctx.stats().particle_kernel_ms
+                sums = ops.finish(ops.all_gather(parts, counts))
+                means = ops.divide(sums, spec.n_particles)
+                ops.finish(ops.all_gather(ops.sq_partials(means, b, e), counts))
+                return k, my_steps
+            return timed(run)
+
+        def e2e_step():
+            if world == 1:
+                return S.observe_ad(spec, 808, ctx=ctx)
+            return D.observe_ad_sharded(spec, 808, rank, world, ctx)
+        api = ("paper_1808_10580_b200.observe_ad -> smc_ad_observe (C ABI)" if world == 1 else
+               "paper_1808_10580_b200.distributed.observe_ad_sharded (C ABI + NCCL all-gather)")
+        parallel = f"particle-shard x{world}" if world > 1 else "single GPU"
+        scaling = "strong"
+        h2d, d2h = _image_bytes(spec), 40 * len(spec.observations)
+        kernel_name = "ad_particles (K1)"
+    elif kind == "bvp":
+        spec = payload
+        n_obs = len(spec.observations)
+        ob, oe = (n_obs * rank) // world, (n_obs * (rank + 1)) // world
+
+        def device_step():
+            def run():
+                S.observe_bvp_range(spec, 606, ob, oe - ob, ctx=ctx)
+                st = ctx.stats()
+                return st.particle_kernel_ms, st.particle_steps
+            return timed(run)
+
+        def e2e_step():
+            return S.observe_bvp_range(spec, 606, ob, oe - ob, ctx=ctx)
+        api = "paper_1808_10580_b200.observe_bvp_range -> smc_bvp_observe_range (C ABI)"
+        parallel = f"observation-shard x{world}" if world > 1 else "single GPU"
+        scaling = "strong"
+        h2d, d2h = 16 * n_obs + 512, 40 * (oe - ob)
+        kernel_name = "bvp_walkers (K2)"
+    else:  # batched
+        base, prior, U = payload
+        sb, se = D.sample_range(len(U), rank, world)
+        my_U = U[sb:se]
+        my_steps = steps_per_eval * (se - sb) / len(U)
+
+        def device_step():
+            def run():
+                S.observe_ad_batched(base, prior, my_U, 808, ctx=ctx)
+                return ctx.stats().particle_kernel_ms, my_steps
+            return timed(run)
+
+        def e2e_step():
+            return S.observe_ad_batched(base, prior, my_U, 808, ctx=ctx)
+        api = "paper_1808_10580_b200.observe_ad_batched -> smc_ad_observe_batched (C ABI)"
+        parallel = f"sample-shard x{world}" if world > 1 else "single GPU"
+        scaling = "strong"
+        h2d, d2h = my_U.nbytes + 2048, 40 * len(base.observations) * len(my_U)
+        kernel_name = "ad_particles<double> generic tiled lattice (K1)"
 
     for _ in range(args.warmup):
         device_step()
@@ -243,20 +385,22 @@ def run_ours(args):
     time.sleep(0.3)
     dev_ms = k_ms = 0.0
     launches = 0
+    my_total_steps = 0.0
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     for _ in range(args.steps):
         flush.zero_()  # L2 flush between timed iterations (outside the step's events)
         torch.cuda.synchronize()
-        d, k, n = device_step()
+        d, k, n, st = device_step()
         dev_ms += d
         k_ms += k
         launches += n
+        my_total_steps += st
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    # end-to-end through the public API (host spec in, host estimates out)
+    # end-to-end through the public API (host inputs in, host estimates out)
     e2e_s = 0.0
     for _ in range(args.steps):
         flush.zero_()
@@ -264,52 +408,46 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        est = e2e_step()
+        e2e_step()
         e2e_s += time.perf_counter() - t0
     torch.cuda.synchronize()
     clocks = sampler.stop()
 
-    t = torch.tensor([dev_ms, k_ms, e2e_s], dtype=torch.float64, device="cuda")
+    tmax = torch.tensor([dev_ms, e2e_s], dtype=torch.float64, device=red_dev)
+    tsum = torch.tensor([my_total_steps], dtype=torch.float64, device=red_dev)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    dev_ms, k_ms, e2e_s = t.tolist()
-
-    total_steps = steps_per_eval * args.steps
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+    dev_ms, e2e_s = tmax.tolist()
+    total_steps = tsum.item()
+    per_eval = total_steps / args.steps
     value = total_steps / (dev_ms / 1e3)
     e2e_value = total_steps / e2e_s
-    local_steps_per_eval = steps_per_eval * (D.chunk_range(D.num_chunks(spec.n_particles), rank, world)[1] -
-                                             D.chunk_range(D.num_chunks(spec.n_particles), rank, world)[0]) / max(
-        1, D.num_chunks(spec.n_particles))
-    achieved = F * local_steps_per_eval * args.steps / (k_ms / 1e3) / 1e12  # per-launch algorithmic flops / duration
-    h2d = _image_bytes(spec)
-    d2h = 40 * len(spec.observations)
+    # roofline: this rank's algorithmic flops over its particle-kernel event time
+    achieved = F * my_total_steps / (k_ms / 1e3) / 1e12
 
     if rank == 0:
-        traffic = _ncu_traffic()
         line = {
             "metric": METRIC, "value": value, "unit": "particle-steps/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (prior-draw velocity, reference recipe)",
-            "config": dict(desc, parallelism=f"particle-shard x{world}" if world > 1 else "single GPU",
-                           l2="flushed between steps (256 MiB write)"),
-            "evals_per_sec": value / steps_per_eval,
-            "e2e": {"value": e2e_value, "unit": "particle-steps/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "evals_per_sec": e2e_value / steps_per_eval,
-                    "api": "paper_1808_10580_b200.observe_ad -> smc_ad_observe (C ABI)" if world == 1 else
-                           "paper_1808_10580_b200.distributed.observe_ad_sharded"},
-            "roofline": {"bound": "fp64", "kernel": "ad_particles<double> (K1)", "achieved": achieved,
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (prior-draw velocity, reference recipe)",
+            "config": dict(desc, parallelism=parallel, l2="flushed between steps (256 MiB write)"),
+            "evals_per_sec": value / per_eval,
+            "e2e": {"value": e2e_value, "unit": "particle-steps/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "evals_per_sec": e2e_value / per_eval, "api": api},
+            "roofline": {"bound": "fp64", "kernel": kernel_name, "achieved": achieved,
                          "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                          "peak_source": "FP64 DFMA microbenchmark measured in this run (smc_fp64_peak, all SMs, "
                                         "8 chains/thread); MEASURED_PEAKS.json has no FP64 entry",
                          "flops_per_unit": F, "unit_of_work": "particle-step",
-                         "traffic": traffic},
+                         "traffic": _ncu_traffic(args.config)},
             "gpu_launches": launches,
             "clocks": clocks,
         }
         if world == 1 and not args.no_cpu_baseline:
             try:
-                v, cores, sample = cpu_reference_sample(spec, steps_per_eval)
+                v, cores, sample = cpu_reference_sample(args.config, ctx, per_eval)
                 line["cpu_baseline"] = {"value": v, "unit": "particle-steps/s", "cores": cores, "kind": "reference",
                                         "sample": sample}
             except Exception as e:  # noqa: BLE001
@@ -332,9 +470,10 @@ def _image_bytes(spec) -> int:
     return int(b)
 
 
-def _ncu_traffic():
-    """DRAM bytes per K1 launch from the committed ncu --set full capture."""
-    caps = sorted(PROFILES.glob("r*_k1_c2.json"))
+def _ncu_traffic(config: str = "c2"):
+    """DRAM bytes per particle-kernel launch from the committed ncu --set full
+    capture of this config (profiles/rNN_k*_<config>.json), if any."""
+    caps = sorted(PROFILES.glob(f"r*_k*_{config}.json"))
     if caps:
         try:
             d = json.loads(caps[-1].read_text())
@@ -348,50 +487,34 @@ def _ncu_traffic():
 # reference arm
 # ---------------------------------------------------------------------------
 def run_reference(args):
+    """The reference's own CPU implementation (oracle/_ref) on all host cores,
+    same config/metric/unit as our arm; each step a bounded sample."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    import copy
-
-    import paper_1808_10580_b200 as S
-    import specs
     from oracle.oracle import Reference
-
     R = Reference()
     cores = os.cpu_count() or 1
-    # same workload as ours; the reference's input recipe, with the reference's
-    # own prior_draw (inference.cpp:55-61) so no GPU is needed on this arm
-    if args.config == "c2":
-        u = R.prior_draw(specs.C2_PRIOR, 808, 0xBE9C4, 0)
-        spec = specs.c2_spec(u, n_particles=100_000)
-        desc = {"workload": "C2: AD forward map, K=8 Fourier velocity (M=98, N_u=197), 9 obs, 1e5 particles/obs, "
-                            "1000 EM steps, FP64", "K": 8, "modes": 98, "n_obs": 9, "particles_per_obs": 100_000,
-                "em_steps": 1000, "seed": 808}
-    else:
-        spec = specs.c1_two_mode()
-        desc = {"workload": "C1: shipped forward_ad_two_mode.json", "K": 1, "modes": 2}
-    steps_per_eval = sum(int(math.ceil(o.t / spec.dt)) for o in spec.observations) * spec.n_particles
-    per_particle = steps_per_eval // spec.n_particles
-    sample = copy.copy(spec)
-    n = int(max(64, min(spec.n_particles, 4.0 * 1.5e6 * cores / per_particle)))  # ~4 s per step
-    sample.n_particles = n
+    kind, payload, steps_full, F, desc = build_workload(
+        args.config, None, u_source=lambda prior, seed, obs, particle: R.prior_draw(prior, seed, obs, particle))
+    steps, run, sample = reference_runner(args.config, R, cores, budget_s=4.0)
     for _ in range(args.warmup):
-        R.observe_ad(sample, 808, cores)
+        run()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        R.observe_ad(sample, 808, cores)
+        run()
     el = time.perf_counter() - t0
-    value = per_particle * n * args.steps / el
+    value = steps * args.steps / el
+    per_eval = steps_full if steps_full else steps
     line = {"metric": METRIC, "impl": "reference", "value": value, "unit": "particle-steps/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (prior-draw velocity, reference recipe)",
             "config": dict(desc, parallelism=f"std::thread x{cores} (reference executor)"),
-            "evals_per_sec": value / steps_per_eval,
+            "evals_per_sec": value / per_eval,
             "cpu_baseline": {"value": value, "unit": "particle-steps/s", "cores": cores, "kind": "reference",
-                             "sample": f"observe_ad with {n} particles/obs (of {spec.n_particles}) per step, "
-                                       f"workers={cores}"},
+                             "sample": sample},
             "e2e": {"value": value, "unit": "particle-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -401,9 +524,12 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c5"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: test the multi-rank path with fewer GPUs than ranks")
+    ap.add_argument("--device", type=int, default=-1, help="override LOCAL_RANK -> device (plumbing tests)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

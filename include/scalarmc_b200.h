@@ -188,6 +188,13 @@ smc_status smc_ad_observe_batched(smc_ctx* ctx, const smc_ad_problem* base, cons
 smc_status smc_bvp_observe(smc_ctx* ctx, const smc_bvp_problem* prob, uint64_t seed,
                            smc_estimate* out);
 
+/* observe_bvp restricted to observations [obs_begin, obs_begin + obs_count)
+ * with their original stream slots (observation sharding across GPUs: the
+ * result for slot j never depends on which rank computes it).
+ * out: [obs_count]. */
+smc_status smc_bvp_observe_range(smc_ctx* ctx, const smc_bvp_problem* prob, uint64_t seed, int64_t obs_begin,
+                                 int64_t obs_count, smc_estimate* out);
+
 /* ---- resolved step sizes (host only, no device needed) ------------------- */
 /* AdProblemSpec::resolved_dt (forward_ad.cpp:10-15). */
 smc_status smc_ad_resolved_dt(const smc_ad_problem* prob, double* out);

@@ -35,6 +35,7 @@ from .api import (  # noqa: F401
     observe_ad_batched,
     observe_ad_single,
     observe_bvp,
+    observe_bvp_range,
     philox_device,
     prior_draw,
     velocity_from_coefficients,

@@ -103,6 +103,8 @@ _PROTOS = {
                                          C.POINTER(smc_estimate)]),
     "smc_bvp_observe": (C.c_int, [C.c_void_p, C.POINTER(smc_bvp_problem), C.c_uint64,
                                   C.POINTER(smc_estimate)]),
+    "smc_bvp_observe_range": (C.c_int, [C.c_void_p, C.POINTER(smc_bvp_problem), C.c_uint64, C.c_int64,
+                                        C.c_int64, C.POINTER(smc_estimate)]),
     "smc_ad_resolved_dt": (C.c_int, [C.POINTER(smc_ad_problem), _dp]),
     "smc_bvp_resolved_dt": (C.c_int, [C.POINTER(smc_bvp_problem), _dp]),
     "smc_ad_validate": (C.c_int, [C.POINTER(smc_ad_problem)]),

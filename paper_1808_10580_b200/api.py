@@ -534,6 +534,17 @@ def observe_bvp(spec: BvpProblemSpec, seed: int, workers: int = 1, ctx: Context 
     return [ParticleEstimate._from(out[j]) for j in range(p.n_obs)]
 
 
+def observe_bvp_range(spec: BvpProblemSpec, seed: int, obs_begin: int, obs_count: int,
+                      ctx: Context | None = None) -> list[ParticleEstimate]:
+    """observe_bvp for observations [obs_begin, obs_begin + obs_count) with
+    their original stream slots (observation sharding across GPUs)."""
+    ctx = ctx or default_context()
+    p, keep = spec._pod()
+    out = (A.smc_estimate * max(obs_count, 1))()
+    _check(ctx.lib.smc_bvp_observe_range(ctx.handle, C.byref(p), C.c_uint64(seed), obs_begin, obs_count, out))
+    return [ParticleEstimate._from(out[j]) for j in range(obs_count)]
+
+
 def observe_ad_batched(spec: AdProblemSpec, prior: "PriorSpec", u: np.ndarray, seed: int,
                        seeds: np.ndarray | None = None, ctx: Context | None = None) -> np.ndarray:
     """Batched AD forward map: row b of u (prior order) -> estimates [B][n_obs]

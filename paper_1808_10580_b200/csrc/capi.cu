@@ -746,12 +746,19 @@ smc_status smc_fp64_peak(smc_ctx* ctx, double ms, double* tflops) {
 }
 
 smc_status smc_bvp_observe(smc_ctx* ctx, const smc_bvp_problem* p, uint64_t seed, smc_estimate* out) {
+    return smc_bvp_observe_range(ctx, p, seed, 0, p->n_obs, out);
+}
+
+smc_status smc_bvp_observe_range(smc_ctx* ctx, const smc_bvp_problem* p, uint64_t seed, int64_t obs_begin,
+                                 int64_t obs_count, smc_estimate* out) {
     return guarded([&] {
+        if (obs_begin < 0 || obs_count < 0 || obs_begin + obs_count > p->n_obs)
+            raise(SMC_ERANGE, "observe_bvp: observation range out of bounds");
         CK(cudaSetDevice(ctx->device));
         ctx->stats = smc_stats{};
-        BvpLaunch L = prepare_bvp(ctx, *p, 0, p->n_obs);
+        BvpLaunch L = prepare_bvp(ctx, *p, obs_begin, obs_count);
         L.seed = seed;
-        const int64_t n = p->n_particles, n_obs = p->n_obs;
+        const int64_t n = p->n_particles, n_obs = obs_count;
         run_bvp(ctx, L, n_obs, n);
         // compaction of valid walkers, then the same tree as AD
         cudaStream_t s = ctx->stream;

@@ -106,17 +106,27 @@ class DeviceOps:
         return sums / float(n)  # IEEE division, same as executor.cpp:103
 
     def all_gather(self, local, counts: list[int]):
+        """Rank-ordered concatenation of every rank's [n_obs][count_r] chunk
+        sums (NCCL all_gather_into_tensor on device buffers; over a gloo group
+        the tensors travel through the host, which the CPU/1-GPU tests use)."""
         torch = self.torch
         import torch.distributed as dist
         world = len(counts)
         if world == 1:
             return local
         width = max(counts)
-        buf = torch.zeros((self.n_obs, width), dtype=torch.float64, device=self.dev)
-        buf[:, : local.shape[1]] = local
-        gathered = torch.empty((world, self.n_obs, width), dtype=torch.float64, device=self.dev)
-        dist.all_gather_into_tensor(gathered, buf, group=self.group)
-        return torch.cat([gathered[r, :, : counts[r]] for r in range(world)], dim=1)
+        on_host = dist.get_backend(self.group) == "gloo"
+        dev = torch.device("cpu") if on_host else self.dev
+        buf = torch.zeros((self.n_obs, width), dtype=torch.float64, device=dev)
+        buf[:, : local.shape[1]] = local.to(dev)
+        if on_host:
+            parts = [torch.empty_like(buf) for _ in range(world)]
+            dist.all_gather(parts, buf, group=self.group)
+            gathered = torch.stack(parts)
+        else:
+            gathered = torch.empty((world, self.n_obs, width), dtype=torch.float64, device=dev)
+            dist.all_gather_into_tensor(gathered, buf, group=self.group)
+        return torch.cat([gathered[r, :, : counts[r]] for r in range(world)], dim=1).to(self.dev)
 
     def to_host(self, t) -> np.ndarray:
         return t.double().cpu().numpy()

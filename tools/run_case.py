@@ -46,6 +46,20 @@ if args.config == "c4":
           f"{st.particle_steps / st.particle_kernel_ms * 1e3:.4g} particle-steps/s; "
           f"{14 * 980 + 12 * 24 + 20} flop/step -> {(14 * 980 + 12 * 24 + 20) * st.particle_steps / st.particle_kernel_ms / 1e9:.2f} TFLOP/s")
     sys.exit(0)
+if args.config in ("c3", "c3b"):
+    # paper BVP, F=(1,-0.5,2), 25 obs, 1e6 walkers/obs, seed 606
+    import specs
+    spec = specs.c3_spec(n_particles=args.particles or 1_000_000, precision=S.Precision[args.precision])
+    if args.config == "c3b":
+        u = S.prior_draw(specs.C2_PRIOR, 808, 0xBE9C4, 0, ctx)
+        spec.velocity = S.VelocityField.fourier(S.velocity_from_coefficients(specs.C2_PRIOR, u))
+    for _ in range(args.reps):
+        est = S.observe_bvp(spec, 606, ctx=ctx)
+    st = ctx.stats()
+    print(f"{args.config}: kernel {st.particle_kernel_ms:.3f} ms reduce {st.reduce_ms:.3f} ms walker-steps "
+          f"{st.particle_steps} -> {st.particle_steps / st.particle_kernel_ms * 1e3:.4g} walker-steps/s; "
+          f"mean[0]={est[0].mean:.15g} exit[0]={est[0].aux_mean:.6g} failed={sum(e.n_failed for e in est)}")
+    sys.exit(0)
 spec, steps, F, desc = bench.build_workload(args.config, ctx)
 if args.cutoff:
     import specs
