@@ -168,10 +168,12 @@ __device__ __forceinline__ void velocity_disk(const SmemCoef<T>& C, const T (&x1
         sincospi_t(T(2) * x2[p], &s2, &c2);
         W.pr[p][1] = c2;
         W.pi[p][1] = s2;
+        // P2[j] = P2[j/2] P2[j - j/2]: dependency depth log2(K) instead of K
 #pragma unroll
         for (int j = 2; j <= K; ++j) {
-            W.pr[p][j] = fma(W.pr[p][j - 1], c2, -W.pi[p][j - 1] * s2);
-            W.pi[p][j] = fma(W.pr[p][j - 1], s2, W.pi[p][j - 1] * c2);
+            const int a = j / 2, b = j - j / 2;
+            W.pr[p][j] = fma(W.pr[p][a], W.pr[p][b], -W.pi[p][a] * W.pi[p][b]);
+            W.pi[p][j] = fma(W.pr[p][a], W.pi[p][b], W.pi[p][a] * W.pr[p][b]);
         }
         W.qr[p][1] = c2;
         W.qi[p][1] = s2;
@@ -194,7 +196,7 @@ __device__ __forceinline__ void velocity_disk(const SmemCoef<T>& C, const T (&x1
 }
 
 template <int K, class T, int P>
-__global__ void __launch_bounds__(kBlock) ad_particles_disk(const AdLaunch L, const DiskCoef<K, T> Pc) {
+__global__ void __launch_bounds__(kBlock, (K <= 8 ? 4 : 3)) ad_particles_disk(const AdLaunch L, const DiskCoef<K, T> Pc) {
     __shared__ __align__(16) T staged[DiskShape<K>::n_coef];
     for (int i = threadIdx.x; i < DiskShape<K>::n_coef; i += kBlock) staged[i] = Pc.c[i];
     __syncthreads();

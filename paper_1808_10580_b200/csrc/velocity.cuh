@@ -13,6 +13,7 @@
 // recurrence, (k1,k2)-sorted mode loop, w = 2 Re(v e), v += w d.
 #pragma once
 
+#include "fastmath.cuh"
 #include "images.h"
 #include "smc_device.cuh"
 
@@ -20,7 +21,7 @@ namespace smc {
 
 constexpr int kLatticeTile = 8;
 
-__device__ __forceinline__ void sincospi_t(double a, double* s, double* c) { sincospi(a, s, c); }
+__device__ __forceinline__ void sincospi_t(double a, double* s, double* c) { fm::sincospi(a, s, c); }
 __device__ __forceinline__ void sincospi_t(float a, float* s, float* c) { sincospif(a, s, c); }
 
 // Four coefficients (alpha_re, alpha_im, beta_re, beta_im) of one pair.
