@@ -10,6 +10,7 @@
 // difference from the reference is libm: CUDA's log/sin/cos vs glibc's.  The
 // parity tests use this kernel to show the per-particle values are bitwise
 // equal to the reference except where libm rounds differently.
+#define SMC_STRICT_TU 1
 #include <cuda_runtime.h>
 
 #include "kernels.h"

@@ -30,7 +30,42 @@ constexpr int kBvpBlock = 128;
 __device__ __forceinline__ double log_u(double x) { return fm::log_pos(x); }  // uniform in (0,1)
 __device__ __forceinline__ float log_u(float x) { return __logf(x); }
 
-template <class T, bool STRICT, int KCAP>
+// Forcing f(x) evaluated every step.  NB > 0: a Gaussian-bump sum of exactly
+// NB terms held in registers for the whole walk (no per-step loads or
+// dispatch); NB == 0: the generic ScalarField evaluator.
+template <int NB>
+struct Forcing {
+    double c1[NB > 0 ? NB : 1], c2[NB > 0 ? NB : 1], amp[NB > 0 ? NB : 1];
+    double neg_a = 0.0;
+    __device__ __forceinline__ explicit Forcing(const ScalarImg& f) {
+        if constexpr (NB > 0) {
+            neg_a = f.neg_sharpness;
+#pragma unroll
+            for (int i = 0; i < NB; ++i) {
+                c1[i] = __ldg(f.center + 2 * i);
+                c2[i] = __ldg(f.center + 2 * i + 1);
+                amp[i] = __ldg(f.amp + i);
+            }
+        }
+    }
+    __device__ __forceinline__ double operator()(const ScalarImg& f, double x1, double x2) const {
+        if constexpr (NB == 0) {
+            return scalar_eval(f, x1, x2);
+        } else {
+            double s = 0.0;  // same order as ScalarField::operator() (fields.cpp:244-248)
+#pragma unroll
+            for (int i = 0; i < NB; ++i) {
+                const double d1 = x1 - c1[i], d2 = x2 - c2[i];
+                s += amp[i] * SMC_SCALAR_EXP(neg_a * (d1 * d1 + d2 * d2));
+            }
+            return s;
+        }
+    }
+};
+
+// VEL: 0 = runtime dispatch (constant or Fourier), 1 = constant velocity
+// only (the lattice series is compiled out, which frees registers).
+template <class T, bool STRICT, int KCAP, int NB = 0, int VEL = 0>
 __global__ void __launch_bounds__(kBvpBlock) bvp_walkers(const BvpLaunch L) {
     constexpr unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
@@ -46,6 +81,7 @@ __global__ void __launch_bounds__(kBvpBlock) bvp_walkers(const BvpLaunch L) {
     T x1 = T(0), x2 = T(0), f_int = T(0);
     unsigned long long my_steps = 0;
     cd p1[STRICT ? KCAP + 1 : 1], p2[STRICT ? KCAP + 1 : 1];
+    const Forcing<NB> forcing(L.forcing);
 
     for (;;) {
         if (!exhausted) {
@@ -87,10 +123,10 @@ __global__ void __launch_bounds__(kBvpBlock) bvp_walkers(const BvpLaunch L) {
                 sincospi_t(T(2) * T(u.u1), &sn, &cs);
                 xi1 = rad * cs;
                 xi2 = rad * sn;
-                if (L.vel.is_constant) {
+                if (VEL == 1 || L.vel.is_constant) {
                     v1 = T(L.vel.c1);
                     v2 = T(L.vel.c2);
-                } else {
+                } else if constexpr (VEL == 0) {
                     velocity_lattice<T, double>(lat, lat.coef, x1, x2, v1, v2);
                 }
             }
@@ -102,7 +138,7 @@ __global__ void __launch_bounds__(kBvpBlock) bvp_walkers(const BvpLaunch L) {
                 n1 = fma(sr, xi1, fma(-v1, dt, x1));
                 n2 = fma(sr, xi2, fma(-v2, dt, x2));
             }
-            const T f = T(scalar_eval(L.forcing, double(x1), double(x2)));
+            const T f = T(forcing(L.forcing, double(x1), double(x2)));
             ++my_steps;
             if (!domain_contains<T>(L.domain, n1, n2)) {
                 T h1, h2;

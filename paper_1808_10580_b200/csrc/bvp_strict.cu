@@ -2,6 +2,7 @@
 // (compiled with -fmad=false): the reference's operation order throughout, so
 // per-walker results differ from the reference only where CUDA's libm rounds
 // differently from glibc's.
+#define SMC_STRICT_TU 1
 #include <cuda_runtime.h>
 
 #include "bvp_body.cuh"

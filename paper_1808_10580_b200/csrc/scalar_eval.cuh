@@ -3,10 +3,19 @@
 // inherits that unit's contraction mode (-fmad=false for the strict path).
 #pragma once
 
+#include "fastmath.cuh"
 #include "images.h"
 #include "../../include/scalarmc_b200.h"
 
 namespace smc {
+
+// The strict translation units keep libdevice exp; the fast ones use the
+// constant-bank fastmath version.
+#ifdef SMC_STRICT_TU
+#define SMC_SCALAR_EXP exp
+#else
+#define SMC_SCALAR_EXP fm::exp_
+#endif
 
 __device__ __forceinline__ double scalar_eval(const ScalarImg& f, double x1, double x2) {
     switch (f.kind) {
@@ -22,7 +31,7 @@ __device__ __forceinline__ double scalar_eval(const ScalarImg& f, double x1, dou
             double s = 0.0;
             for (int i = 0; i < f.n; ++i) {
                 const double d1 = x1 - __ldg(f.center + 2 * i), d2 = x2 - __ldg(f.center + 2 * i + 1);
-                s += __ldg(f.amp + i) * exp(f.neg_sharpness * (d1 * d1 + d2 * d2));
+                s += __ldg(f.amp + i) * SMC_SCALAR_EXP(f.neg_sharpness * (d1 * d1 + d2 * d2));
             }
             return s;
         }
