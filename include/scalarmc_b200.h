@@ -195,6 +195,41 @@ smc_status smc_bvp_observe(smc_ctx* ctx, const smc_bvp_problem* prob, uint64_t s
 smc_status smc_bvp_observe_range(smc_ctx* ctx, const smc_bvp_problem* prob, uint64_t seed, int64_t obs_begin,
                                  int64_t obs_count, smc_estimate* out);
 
+/* ---- device-resident multi-chain pCN ------------
+ * run_chain (include/scalarmc/inference.hpp:95-99, src/inference.cpp:170-194)
+ * for n_chains independent chains at once: every step evaluates all chains'
+ * proposals with ONE batched forward map (common random numbers:
+ * forward_seed, as LikelihoodSpec::misfit), and the proposal draw, the
+ * u -> field packing, Phi, the accept/reject and the MAP tracking stay on the
+ * device.  Chain c uses the stream NormalStream{chain_seeds[c], 0xFFFFFFFF, 0}
+ * exactly as run_chain does with config.seed (inference.cpp:12, :175), so
+ * chain c reproduces run_chain(config with seed = chain_seeds[c]).
+ * `forward` is the likelihood's AdProblemSpec (its velocity slot is ignored);
+ * data: [n_obs] (LikelihoodSpec::data); u0: [n_chains][dim] or NULL (draw from
+ * the prior).  Output arrays are caller-owned; any may be NULL except
+ * final_u. */
+typedef struct smc_chain_config { /* ChainConfig (inference.hpp:87-93) */
+    int64_t n_steps;
+    double beta;
+    int64_t burn_in;
+    int64_t thin;
+} smc_chain_config;
+
+typedef struct smc_chain_outputs {
+    double* final_u;        /* [n_chains][dim] */
+    double* final_phi;      /* [n_chains] */
+    double* map_u;          /* [n_chains][dim] */
+    double* map_objective;  /* [n_chains] */
+    int64_t* accepted;      /* [n_chains] */
+    double* phi_trace;      /* [n_chains][n_steps] */
+    double* samples;        /* [n_chains][smc_pcn_num_samples(cfg)][dim] */
+} smc_chain_outputs;
+
+int64_t smc_pcn_num_samples(const smc_chain_config* cfg);
+smc_status smc_pcn_chains(smc_ctx* ctx, const smc_ad_problem* forward, const smc_prior* prior, const double* data,
+                          double noise_std, uint64_t forward_seed, int64_t n_chains, const uint64_t* chain_seeds,
+                          const double* u0, const smc_chain_config* cfg, smc_chain_outputs* out);
+
 /* ---- resolved step sizes (host only, no device needed) ------------------- */
 /* AdProblemSpec::resolved_dt (forward_ad.cpp:10-15). */
 smc_status smc_ad_resolved_dt(const smc_ad_problem* prob, double* out);

@@ -230,6 +230,29 @@ class Reference(_Checker):
         _status(self.lib, self.prefix, rc)
         return out.value
 
+    def run_chain(self, like, prior, n_steps: int, beta: float, burn_in: int, thin: int, seed: int, u0=None,
+                  workers: int = 0) -> dict:
+        """The reference's run_chain (inference.cpp:170-194) with LikelihoodSpec
+        `like` (paper_1808_10580_b200.LikelihoodSpec)."""
+        p, keep = like.forward._pod()
+        dim = prior.dimension()
+        n_samples = max(0, (n_steps - max(burn_in, 0) - 1) // thin + 1) if n_steps > burn_in else 0
+        trace = np.zeros(max(n_steps, 1))
+        samples = np.zeros((max(n_samples, 1), dim))
+        final_u = np.zeros(dim)
+        map_u = np.zeros(dim)
+        sc = np.zeros(3)
+        d = np.ascontiguousarray(like.data, dtype=np.float64)
+        u0p = np.ascontiguousarray(u0, dtype=np.float64).ctypes.data_as(_dp) if u0 is not None else _dp()
+        rc = self.lib.ref_run_chain(C.byref(p), C.byref(prior._pod()), d.ctypes.data_as(_dp),
+                                    C.c_double(like.noise_std), C.c_uint64(like.forward_seed), C.c_int64(n_steps),
+                                    C.c_double(beta), C.c_int64(burn_in), C.c_int64(thin), C.c_uint64(seed), u0p,
+                                    C.c_int(workers), trace.ctypes.data_as(_dp), samples.ctypes.data_as(_dp),
+                                    final_u.ctypes.data_as(_dp), map_u.ctypes.data_as(_dp), sc.ctypes.data_as(_dp))
+        _status(self.lib, self.prefix, rc)
+        return {"phi_trace": trace[:n_steps], "samples": samples[:n_samples], "final_u": final_u, "map_u": map_u,
+                "final_phi": sc[0], "map_objective": sc[1], "accepted": int(sc[2])}
+
     def resolved_dt_ad(self, spec) -> float:
         p, keep = spec._pod()
         out = C.c_double()

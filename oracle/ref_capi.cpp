@@ -14,6 +14,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -311,6 +312,44 @@ int ref_forcing_cost(const smc_bvp_problem* base, int64_t n_bumps, const double*
         c.target.assign(target, target + base->n_obs);
         *out = forcing_cost(std::span<const double>(amplitudes, static_cast<std::size_t>(n_bumps)), c, b,
                             seed, workers);
+    });
+}
+
+// run_chain (inference.cpp:170-194), unchanged reference code.  Outputs:
+// phi_trace [n_steps], samples [n_samples][dim], final_u [dim], map_u [dim],
+// scalars[0..2] = (final phi, map objective, accepted).
+int ref_run_chain(const smc_ad_problem* base, const smc_prior* prior, const double* data, double noise_std,
+                  uint64_t forward_seed, int64_t n_steps, double beta, int64_t burn_in, int64_t thin, uint64_t seed,
+                  const double* u0, int workers, double* phi_trace, double* samples, double* final_u, double* map_u,
+                  double* scalars) {
+    return guarded([&] {
+        const PriorSpec ps{prior->cutoff, prior->s0, prior->alpha};
+        LikelihoodSpec like;
+        like.forward = to_ad(*base);
+        like.data.assign(data, data + base->n_obs);
+        like.noise_std = noise_std;
+        like.forward_seed = forward_seed;
+        like.workers = workers;
+        ChainConfig cc;
+        cc.n_steps = n_steps;
+        cc.beta = beta;
+        cc.burn_in = burn_in;
+        cc.thin = thin;
+        cc.seed = seed;
+        std::optional<std::vector<double>> start;
+        const std::size_t dim = static_cast<std::size_t>(ps.dimension());
+        if (u0) start = std::vector<double>(u0, u0 + dim);
+        const ChainResult r = run_chain(cc, ps, &like, start);
+        for (std::size_t i = 0; i < r.phi_trace.size(); ++i) phi_trace[i] = r.phi_trace[i];
+        for (std::size_t k = 0; k < r.samples.size(); ++k)
+            for (std::size_t i = 0; i < dim; ++i) samples[k * dim + i] = r.samples[k][i];
+        for (std::size_t i = 0; i < dim; ++i) {
+            final_u[i] = r.final_state.u[i];
+            map_u[i] = r.map_u[i];
+        }
+        scalars[0] = r.final_state.phi;
+        scalars[1] = r.map_objective;
+        scalars[2] = static_cast<double>(r.final_state.accepted);
     });
 }
 

@@ -8,6 +8,7 @@ from .api import (  # noqa: F401
     AdObservation,
     AdProblemSpec,
     Bump,
+    ChainConfig,
     BvpProblemSpec,
     Context,
     CosineTerm,
@@ -38,6 +39,7 @@ from .api import (  # noqa: F401
     observe_bvp_range,
     philox_device,
     prior_draw,
+    run_chains,
     velocity_from_coefficients,
 )
 from ._abi import LIB_PATH, load_library  # noqa: F401

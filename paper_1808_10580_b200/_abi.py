@@ -66,6 +66,15 @@ class smc_prior(C.Structure):
     _fields_ = [("cutoff", C.c_int32), ("pad_", C.c_int32), ("s0", C.c_double), ("alpha", C.c_double)]
 
 
+class smc_chain_config(C.Structure):
+    _fields_ = [("n_steps", C.c_int64), ("beta", C.c_double), ("burn_in", C.c_int64), ("thin", C.c_int64)]
+
+
+class smc_chain_outputs(C.Structure):
+    _fields_ = [("final_u", _dp), ("final_phi", _dp), ("map_u", _dp), ("map_objective", _dp),
+                ("accepted", C.POINTER(C.c_int64)), ("phi_trace", _dp), ("samples", _dp)]
+
+
 class smc_stats(C.Structure):
     _fields_ = [("particle_kernel_ms", C.c_double), ("reduce_ms", C.c_double),
                 ("kernel_launches", C.c_int64), ("particle_steps", C.c_int64),
@@ -105,6 +114,10 @@ _PROTOS = {
                                   C.POINTER(smc_estimate)]),
     "smc_bvp_observe_range": (C.c_int, [C.c_void_p, C.POINTER(smc_bvp_problem), C.c_uint64, C.c_int64,
                                         C.c_int64, C.POINTER(smc_estimate)]),
+    "smc_pcn_num_samples": (C.c_int64, [C.POINTER(smc_chain_config)]),
+    "smc_pcn_chains": (C.c_int, [C.c_void_p, C.POINTER(smc_ad_problem), C.POINTER(smc_prior), _dp, C.c_double,
+                                 C.c_uint64, C.c_int64, C.POINTER(C.c_uint64), _dp, C.POINTER(smc_chain_config),
+                                 C.POINTER(smc_chain_outputs)]),
     "smc_ad_resolved_dt": (C.c_int, [C.POINTER(smc_ad_problem), _dp]),
     "smc_bvp_resolved_dt": (C.c_int, [C.POINTER(smc_bvp_problem), _dp]),
     "smc_ad_validate": (C.c_int, [C.POINTER(smc_ad_problem)]),

@@ -703,6 +703,52 @@ class LikelihoodSpec:
 
 
 @dataclass
+class ChainConfig:
+    """ChainConfig (inference.hpp:87-93)."""
+    n_steps: int = 10000
+    beta: float = 0.02
+    burn_in: int = 0
+    thin: int = 1
+    seed: int = 0
+
+
+def run_chains(config: ChainConfig, prior: PriorSpec, likelihood: LikelihoodSpec, seeds: Sequence[int],
+               u0: np.ndarray | None = None, keep_samples: bool = True, keep_trace: bool = True,
+               ctx: Context | None = None) -> dict:
+    """len(seeds) independent pCN chains on the device (run_chain,
+    inference.cpp:170-194): chain c is run_chain(config with seed=seeds[c]),
+    and every step evaluates all chains' proposals in one batched forward
+    map.  Returns arrays: final_u [B][dim], final_phi [B], map_u [B][dim],
+    map_objective [B], accepted [B], acceptance_rate [B], phi_trace
+    [B][n_steps], samples [B][n_samples][dim]."""
+    ctx = ctx or default_context()
+    likelihood.validate()
+    p, keep = likelihood.forward._pod()
+    seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+    B, dim = len(seeds), prior.dimension()
+    cfg = A.smc_chain_config(config.n_steps, config.beta, config.burn_in, config.thin)
+    ns = int(ctx.lib.smc_pcn_num_samples(C.byref(cfg)))
+    res = {"final_u": np.zeros((B, dim)), "final_phi": np.zeros(B), "map_u": np.zeros((B, dim)),
+           "map_objective": np.zeros(B), "accepted": np.zeros(B, dtype=np.int64)}
+    res["phi_trace"] = np.zeros((B, max(config.n_steps, 1))) if keep_trace else None
+    res["samples"] = np.zeros((B, max(ns, 1), dim)) if keep_samples and ns > 0 else None
+    out = A.smc_chain_outputs(A.dptr(res["final_u"]), A.dptr(res["final_phi"]), A.dptr(res["map_u"]),
+                              A.dptr(res["map_objective"]), res["accepted"].ctypes.data_as(C.POINTER(C.c_int64)),
+                              A.dptr(res["phi_trace"]), A.dptr(res["samples"]))
+    d = np.ascontiguousarray(likelihood.data, dtype=np.float64)
+    u0p = A.dptr(np.ascontiguousarray(u0, dtype=np.float64).reshape(B, dim)) if u0 is not None else A.dptr(None)
+    _check(ctx.lib.smc_pcn_chains(ctx.handle, C.byref(p), C.byref(prior._pod()), A.dptr(d),
+                                  C.c_double(likelihood.noise_std), C.c_uint64(likelihood.forward_seed), B,
+                                  seeds.ctypes.data_as(C.POINTER(C.c_uint64)), u0p, C.byref(cfg), C.byref(out)))
+    if keep_trace:
+        res["phi_trace"] = res["phi_trace"][:, : config.n_steps]
+    if res["samples"] is not None:
+        res["samples"] = res["samples"][:, :ns]
+    res["acceptance_rate"] = res["accepted"] / max(config.n_steps, 1) if config.n_steps > 0 else np.zeros(B)
+    return res
+
+
+@dataclass
 class ForcingControl:
     """ForcingControl (optimize.hpp:45-54)."""
     initial_amplitudes: list

@@ -22,6 +22,10 @@
 #include "host_problem.h"
 #include "kernels.h"
 
+namespace {
+constexpr int kLatticeTileHost = 8;  // == kLatticeTile (velocity.cuh) / kTileW (host_problem.cpp)
+}
+
 using namespace smc;
 
 namespace {
@@ -302,6 +306,24 @@ void run_particles(smc_ctx* ctx, AdLaunch& L, const AdPrepared* P = nullptr) {
 }
 
 // Reduce [n_seg][n] values (no failures) into estimates on the host.
+// Reduce [n_seg][n] values (no failures) into estimates left on the device.
+smc_estimate* reduce_ad_device(smc_ctx* ctx, const double* values, int64_t n, int64_t n_seg) {
+    cudaStream_t s = ctx->stream;
+    const int64_t chunks = (n + kChunk - 1) / kChunk;
+    double* scratch = ctx->scratch.get<double>(static_cast<size_t>(2 * n_seg * std::max<int64_t>(chunks, 1)));
+    double* sums = ctx->sums.get<double>(static_cast<size_t>(n_seg));
+    double* means = ctx->means.get<double>(static_cast<size_t>(n_seg));
+    double* sumsq = ctx->sumsq.get<double>(static_cast<size_t>(n_seg));
+    smc_estimate* est = ctx->est.get<smc_estimate>(static_cast<size_t>(n_seg));
+    int launches = 0;
+    CK(tree_reduce(values, n, nullptr, n, n_seg, sums, nullptr, 0, scratch, s, &launches));
+    CK(launch_divide(sums, nullptr, n, n_seg, means, s));
+    CK(tree_reduce(values, n, nullptr, n, n_seg, sumsq, means, 1, scratch, s, &launches));
+    CK(launch_estimates(means, sumsq, nullptr, nullptr, n, n, n_seg, est, s));
+    count_launches(ctx, launches + 2);
+    return est;
+}
+
 void reduce_ad(smc_ctx* ctx, const double* values, int64_t n, int64_t n_seg, smc_estimate* out) {
     cudaStream_t s = ctx->stream;
     const int64_t chunks = (n + kChunk - 1) / kChunk;
@@ -742,6 +764,248 @@ smc_status smc_fp64_peak(smc_ctx* ctx, double ms, double* tflops) {
         }
         const double flops = 2.0 * 8.0 * double(iters) * 256.0 * blocks;
         *tflops = flops / (double(t) * 1e-3) / 1e12;
+    });
+}
+
+int64_t smc_pcn_num_samples(const smc_chain_config* cfg) {
+    // iterations i = 1..n_steps with i > burn_in and (i - burn_in - 1) % thin == 0
+    if (!cfg || cfg->thin < 1 || cfg->n_steps <= cfg->burn_in) return 0;
+    const int64_t burn = cfg->burn_in < 0 ? 0 : cfg->burn_in;
+    return (cfg->n_steps - burn - 1) / cfg->thin + 1;
+}
+
+smc_status smc_pcn_chains(smc_ctx* ctx, const smc_ad_problem* forward, const smc_prior* prior, const double* data,
+                          double noise_std, uint64_t forward_seed, int64_t n_chains, const uint64_t* chain_seeds,
+                          const double* u0, const smc_chain_config* cfg, smc_chain_outputs* out) {
+    return guarded([&] {
+        CK(cudaSetDevice(ctx->device));
+        // run_chain's checks (inference.cpp:172-173), prior_draw/chain_init's
+        // (inference.cpp:17-21, :89-91, :125-133), pcn_step's (:138).
+        if (cfg->n_steps < 0) raise(SMC_EINVAL, "run_chain: n_steps must be >= 0");
+        if (cfg->thin < 1) raise(SMC_EINVAL, "run_chain: thin must be >= 1");
+        if (prior->cutoff < 1) raise(SMC_EINVAL, "PriorSpec: cutoff must be >= 1");
+        if (!(prior->s0 >= 0.0)) raise(SMC_EINVAL, "PriorSpec: s0 must be >= 0");
+        if (!std::isfinite(prior->alpha)) raise(SMC_EINVAL, "PriorSpec: alpha must be finite");
+        if (!(noise_std > 0.0)) raise(SMC_EINVAL, "LikelihoodSpec: noise_std must be positive");
+        if (cfg->n_steps > 0 && !(cfg->beta > 0.0 && cfg->beta <= 1.0))
+            raise(SMC_EINVAL, "pcn_step: beta must be in (0,1]");
+        if (n_chains < 1) raise(SMC_EINVAL, "pcn_chains: need at least one chain");
+        if (!out || !out->final_u) raise(SMC_EINVAL, "pcn_chains: final_u output is required");
+        smc_ad_problem p = *forward;
+        check_kappa(p.kappa);
+        check_scalar(p.initial_condition);
+        ad_validate(p);
+        check_particle_range(p.n_particles);
+        if (p.precision == SMC_FP64_STRICT) raise(SMC_EINVAL, "strict precision is single-sample only");
+        cudaStream_t s = ctx->stream;
+        const int64_t n_obs = p.n_obs, n = p.n_particles, B = n_chains;
+
+        // prior modes (|k|^2 then (k1,k2) order) and per-mode stds (inference.cpp:24-53)
+        const std::vector<HostMode> pm = prior_modes(prior->cutoff);
+        const int64_t M = static_cast<int64_t>(pm.size()), dim = 2 * M;
+        std::vector<double> stds(static_cast<size_t>(M));
+        for (int64_t i = 0; i < M; ++i) {
+            const double kn = std::sqrt(double(pm[i].k1) * pm[i].k1 + double(pm[i].k2) * pm[i].k2);
+            stds[static_cast<size_t>(i)] = prior->s0 * std::pow(kn, -prior->alpha);
+        }
+        // lattice structure of the full prior disk and the u -> block gather map
+        PreparedVelocity structure;
+        structure.is_constant = false;
+        structure.K = prior->cutoff;
+        for (const auto& m : pm) structure.modes.push_back(HostMode{m.k1, m.k2, 1.0, 0.0});
+        std::sort(structure.modes.begin(), structure.modes.end(), [](const HostMode& a, const HostMode& b) {
+            return a.k1 != b.k1 ? a.k1 < b.k1 : a.k2 < b.k2;
+        });
+        const LatticeHost Lh = lattice_structure(structure);
+        const int64_t stride = Lh.stride;
+        std::vector<int32_t> ip(static_cast<size_t>(stride), -1), imv(static_cast<size_t>(stride), -1);
+        std::vector<double> sp(static_cast<size_t>(stride), 0.0), sm(static_cast<size_t>(stride), 0.0);
+        {
+            const int K = prior->cutoff;
+            std::vector<int32_t> idx(static_cast<size_t>((K + 1) * (2 * K + 1)), -1);
+            auto at = [&](int k1, int k2) -> int32_t& { return idx[static_cast<size_t>(k1 * (2 * K + 1) + k2 + K)]; };
+            for (int64_t i = 0; i < M; ++i) at(pm[i].k1, pm[i].k2) = static_cast<int32_t>(i);
+            auto g = [&](int k1, int k2) { return 2.0 / std::sqrt(double(k1) * k1 + double(k2) * k2); };
+            auto set = [&](int64_t slot, int k1p, int k2p, int k1m, int k2m, int part, double msign) {
+                if (k2p <= K && k2p >= -K && at(k1p, k2p) >= 0) {
+                    ip[slot] = 2 * at(k1p, k2p) + part;
+                    sp[slot] = g(k1p, k2p);
+                }
+                if (k1m >= 0 && k2m <= K && k2m >= -K && at(k1m, k2m) >= 0) {
+                    imv[slot] = 2 * at(k1m, k2m) + part;
+                    sm[slot] = msign * g(k1m, k2m);
+                }
+            };
+            for (int t = 0; t < Lh.n_tiles; ++t) {
+                const int2 tl = Lh.tiles[static_cast<size_t>(t)];
+                for (int k1 = 1; k1 <= tl.x; ++k1)
+                    for (int q = 0; q < kLatticeTileHost; ++q) {
+                        const int j = kLatticeTileHost * t + q + 1;
+                        if (j > K) break;
+                        const int64_t base = tl.y + static_cast<int64_t>(k1 - 1) * kLatticeTileHost * 4 + 4 * q;
+                        set(base + 0, k1, j, k1, -j, 0, 1.0);   // alpha_re
+                        set(base + 1, k1, j, k1, -j, 1, 1.0);   // alpha_im
+                        set(base + 2, k1, j, k1, -j, 0, -1.0);  // beta_re
+                        set(base + 3, k1, j, k1, -j, 1, -1.0);  // beta_im
+                    }
+            }
+            for (int j = 1; j <= Lh.J0; ++j) {
+                set(Lh.row0_off + 2 * (j - 1), 0, j, -1, 0, 0, 0.0);
+                set(Lh.row0_off + 2 * (j - 1) + 1, 0, j, -1, 0, 1, 0.0);
+            }
+            for (int k1 = 1; k1 <= Lh.R; ++k1) {
+                set(Lh.g0_off + 2 * k1, k1, 0, -1, 0, 0, 0.0);
+                set(Lh.g0_off + 2 * k1 + 1, k1, 0, -1, 0, 1, 0.0);
+            }
+        }
+        if (static_cast<int64_t>(p.n_obs) <= 0) raise(SMC_EINVAL, "AdProblemSpec: no observations");
+
+        // device buffers (freed at the end of the call)
+        std::vector<void*> owned;
+        auto dalloc = [&](size_t bytes) {
+            void* q = nullptr;
+            CK(cudaMalloc(&q, std::max<size_t>(bytes, 16)));
+            owned.push_back(q);
+            return q;
+        };
+        struct Freer {
+            std::vector<void*>* v;
+            ~Freer() {
+                for (void* q : *v) cudaFree(q);
+            }
+        } freer{&owned};
+        auto h2d = [&](void* dst, const void* src, size_t bytes) {
+            CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+        };
+        const int64_t n_samples = smc_pcn_num_samples(cfg);
+        PcnStep S{};
+        S.n_chains = B;
+        S.dim = dim;
+        S.M = M;
+        S.n_obs = n_obs;
+        S.n_steps = cfg->n_steps;
+        S.n_samples = n_samples;
+        S.noise_std = noise_std;
+        S.noise_inf = std::isinf(noise_std) ? 1 : 0;
+        auto* d_stds = static_cast<double*>(dalloc(8 * M));
+        h2d(d_stds, stds.data(), 8 * M);
+        S.stds = d_stds;
+        auto* d_seeds = static_cast<uint64_t*>(dalloc(8 * B));
+        h2d(d_seeds, chain_seeds, 8 * B);
+        S.seeds = d_seeds;
+        auto* d_data = static_cast<double*>(dalloc(8 * n_obs));
+        h2d(d_data, data, 8 * n_obs);
+        S.data = d_data;
+        auto* d_ip = static_cast<int32_t*>(dalloc(4 * stride));
+        auto* d_im = static_cast<int32_t*>(dalloc(4 * stride));
+        auto* d_sp = static_cast<double*>(dalloc(8 * stride));
+        auto* d_sm = static_cast<double*>(dalloc(8 * stride));
+        h2d(d_ip, ip.data(), 4 * stride);
+        h2d(d_im, imv.data(), 4 * stride);
+        h2d(d_sp, sp.data(), 8 * stride);
+        h2d(d_sm, sm.data(), 8 * stride);
+        S.U = static_cast<double*>(dalloc(8 * B * dim));
+        S.Up = static_cast<double*>(dalloc(8 * B * dim));
+        S.map_u = static_cast<double*>(dalloc(8 * B * dim));
+        S.norm_prop = static_cast<double*>(dalloc(8 * B));
+        S.norm_cur = static_cast<double*>(dalloc(8 * B));
+        S.phi = static_cast<double*>(dalloc(8 * B));
+        S.map_obj = static_cast<double*>(dalloc(8 * B));
+        S.accepted = static_cast<int64_t*>(dalloc(8 * B));
+        S.acc_flag = static_cast<uint8_t*>(dalloc(B));
+        S.map_flag = static_cast<uint8_t*>(dalloc(B));
+        S.phi_trace = out->phi_trace ? static_cast<double*>(dalloc(8 * B * std::max<int64_t>(1, cfg->n_steps))) : nullptr;
+        S.samples = (out->samples && n_samples > 0) ? static_cast<double*>(dalloc(8 * B * n_samples * dim)) : nullptr;
+        auto* d_blocks = static_cast<double*>(dalloc(8 * B * stride));
+        CK(cudaMemsetAsync(S.U, 0, 8 * B * dim, s));
+        CK(cudaMemsetAsync(S.accepted, 0, 8 * B, s));
+        CK(cudaMemsetAsync(S.phi, 0, 8 * B, s));
+
+        // forward image (theta_0, observations, lattice tiles); coefficient
+        // blocks come from the pack kernel
+        p.velocity.is_constant = 0;
+        p.velocity.max_wavenumber = prior->cutoff;
+        AdPrepared P = prepare_ad(ctx, p, {&structure}, structure, 0, n_obs);
+        P.L.seed = forward_seed;
+        P.L.seeds = nullptr;
+        P.L.vel.lat.coef = d_blocks;
+        P.L.vel.lat.sample_stride = stride;
+        double* values = ctx->values.get<double>(static_cast<size_t>(B * n_obs * n));
+
+        auto forward_map = [&]() -> smc_estimate* {
+            CK(launch_pcn_pack(d_ip, d_im, d_sp, d_sm, stride, S.Up, dim, B, d_blocks, s));
+            constexpr int64_t kMaxZ = 65535;
+            for (int64_t b0 = 0; b0 < B; b0 += kMaxZ) {
+                AdLaunch L = P.L;
+                L.n_samples = static_cast<int32_t>(std::min(kMaxZ, B - b0));
+                L.vel.lat.coef = d_blocks + b0 * stride;
+                L.values = values + b0 * n_obs * n;
+                run_particles(ctx, L);
+            }
+            count_launches(ctx, 1);
+            return reduce_ad_device(ctx, values, n, B * n_obs);
+        };
+
+        // chain_init (inference.cpp:125-134): u0 given, or prior_draw from the stream
+        uint64_t blk = 0;
+        if (u0) {
+            h2d(S.U, u0, 8 * B * dim);
+            S.contraction = 1.0;  // Up = 1 U + 0 xi = U
+            S.beta = 0.0;
+        } else {
+            S.contraction = 0.0;  // Up = 0 U + 1 xi = xi = prior_draw
+            S.beta = 1.0;
+            blk = static_cast<uint64_t>(M);
+        }
+        S.blk0 = 0;
+        S.init = 1;
+        S.step = 0;
+        S.sample_slot = -1;
+        CK(launch_pcn_propose(S, s));
+        CK(launch_pcn_accept(S, forward_map(), s));
+        CK(launch_pcn_commit(S, s));
+        count_launches(ctx, 3);
+
+        // the steps (pcn_step, inference.cpp:136-166; run_chain loop :182-189)
+        S.init = 0;
+        S.contraction = std::sqrt(1.0 - cfg->beta * cfg->beta);
+        S.beta = cfg->beta;
+        bool ucache = false;
+        uint64_t ublk = 0;
+        for (int64_t it = 0; it < cfg->n_steps; ++it) {
+            S.blk0 = blk;
+            blk += static_cast<uint64_t>(M);
+            if (!ucache) {  // uniform() draws a fresh block and caches its second value
+                ublk = blk;
+                blk += 1;
+                S.uhalf = 0;
+                ucache = true;
+            } else {
+                S.uhalf = 1;
+                ucache = false;
+            }
+            S.ublk = ublk;
+            S.step = it;
+            const int64_t iteration = it + 1;
+            S.sample_slot = (iteration > cfg->burn_in && (iteration - cfg->burn_in - 1) % cfg->thin == 0)
+                                ? (iteration - std::max<int64_t>(cfg->burn_in, 0) - 1) / cfg->thin
+                                : -1;
+            CK(launch_pcn_propose(S, s));
+            CK(launch_pcn_accept(S, forward_map(), s));
+            CK(launch_pcn_commit(S, s));
+            count_launches(ctx, 3);
+        }
+        auto d2h = [&](void* dst, const void* src, size_t bytes) {
+            if (dst) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+        };
+        d2h(out->final_u, S.U, 8 * B * dim);
+        d2h(out->final_phi, S.phi, 8 * B);
+        d2h(out->map_u, S.map_u, 8 * B * dim);
+        d2h(out->map_objective, S.map_obj, 8 * B);
+        d2h(out->accepted, S.accepted, 8 * B);
+        if (S.phi_trace && cfg->n_steps > 0) d2h(out->phi_trace, S.phi_trace, 8 * B * cfg->n_steps);
+        if (S.samples) d2h(out->samples, S.samples, 8 * B * n_samples * dim);
+        CK(cudaStreamSynchronize(s));
     });
 }
 

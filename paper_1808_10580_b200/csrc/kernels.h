@@ -100,6 +100,41 @@ cudaError_t launch_estimates(const double* means, const double* sumsq, const dou
                              const int64_t* counts, int64_t n_uniform, int64_t n_particles,
                              int64_t n_seg, void* out_estimates, cudaStream_t s);
 
+// Device-resident multi-chain pCN (pcn_kernels.cu).
+struct PcnStep {
+    int64_t n_chains, dim, M, n_obs, n_steps, n_samples;
+    const double* stds;      // [M] per-mode prior std (PriorSpec::component_stds, pairwise)
+    double contraction, beta;
+    const uint64_t* seeds;   // [n_chains] chain seeds
+    uint64_t blk0;           // first stream block of this step's prior draw
+    uint64_t ublk;           // block of this step's uniform
+    int32_t uhalf;           // which of its two uniforms
+    int32_t init;            // 1: chain_init (accept the proposal unconditionally)
+    int32_t noise_inf;       // noise_std infinite: Phi == 0
+    int32_t pad_;
+    double noise_std;
+    const double* data;      // [n_obs]
+    double* U;               // [n_chains][dim] state
+    double* Up;              // [n_chains][dim] proposal
+    double* norm_prop;       // [n_chains]
+    double* norm_cur;
+    double* phi;
+    double* map_obj;
+    int64_t* accepted;
+    uint8_t* acc_flag;
+    uint8_t* map_flag;
+    double* map_u;           // [n_chains][dim]
+    double* phi_trace;       // [n_chains][n_steps] or null
+    double* samples;         // [n_chains][n_samples][dim] or null
+    int64_t step;            // 0-based step index
+    int64_t sample_slot;     // >= 0: store the state as sample #slot
+};
+cudaError_t launch_pcn_propose(const PcnStep& S, cudaStream_t s);
+cudaError_t launch_pcn_pack(const int32_t* ip, const int32_t* im, const double* sp, const double* sm, int64_t stride,
+                            const double* Up, int64_t dim, int64_t n_chains, double* blocks, cudaStream_t s);
+cudaError_t launch_pcn_accept(const PcnStep& S, const void* est, cudaStream_t s);
+cudaError_t launch_pcn_commit(const PcnStep& S, cudaStream_t s);
+
 // Diagnostics / microbenchmarks.
 cudaError_t launch_philox(int64_t n, const uint32_t* ctr, const uint32_t* key, uint32_t* out,
                           cudaStream_t s);

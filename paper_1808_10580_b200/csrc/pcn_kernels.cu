@@ -1,0 +1,154 @@
+// pcn_kernels.cu — device-resident multi-chain pCN (compiled with
+// -fmad=false so the chain arithmetic keeps the reference's operation order).
+//
+// One pCN step of B chains (pcn_step, src/inference.cpp:136-166) is
+//   propose (prior_draw + sqrt(1-b^2) u + b xi, prior norm of the proposal)
+//   -> pack (u -> lattice coefficient blocks, velocity_from_coefficients,
+//      inference.cpp:63-73, on the device)
+//   -> K1 batched forward map + K3 reduction (LikelihoodSpec::misfit's
+//      observe_ad, inference.cpp:93-104)
+//   -> accept (Phi, the chain's uniform, min(1, e^{Phi - Phi'}), MAP tracking)
+//   -> commit (state, MAP and thinned-sample copies).
+// The chain randomness is each chain's own NormalStream{seed, 0xFFFFFFFF, 0}
+// (inference.cpp:12, :175): the host tracks the stream's block counter and the
+// uniform() cache (rng.cpp:85-94) — identical for every chain — and passes the
+// block indices to the kernels.
+#define SMC_STRICT_TU 1
+#include <cuda_runtime.h>
+
+#include "../../include/scalarmc_b200.h"
+#include "fastmath.cuh"
+#include "kernels.h"
+#include "smc_device.cuh"
+
+namespace smc {
+namespace {
+
+constexpr uint32_t kChainTag = 0xFFFFFFFFu;  // inference.cpp:12
+
+__device__ __forceinline__ void chain_normals(uint64_t seed, uint64_t block, double& z1, double& z2) {
+    const Uniform2 u = uniform_block(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32), kChainTag, 0u,
+                                     block);
+    const double r = sqrt(-2.0 * fm::log_pos(u.u0));
+    double sn, cs;
+    fm::sincospi(2.0 * u.u1, &sn, &cs);
+    z1 = r * cs;
+    z2 = r * sn;
+}
+
+// xi = prior_draw (stds[i] * normal(), normals pairwise, rng.cpp:74-83),
+// Up = contraction * U + beta * xi (inference.cpp:141-144), and the prior
+// norm 0.5 sum (Up_i / s_i)^2 (inference.cpp:75-83) in the reference's order.
+__global__ void pcn_propose_kernel(PcnStep S) {
+    const int64_t b = blockIdx.x;
+    const uint64_t seed = S.seeds[b];
+    const double* U = S.U + b * S.dim;
+    double* Up = S.Up + b * S.dim;
+    for (int64_t i = threadIdx.x; i < S.M; i += blockDim.x) {
+        double z1, z2;
+        chain_normals(seed, S.blk0 + static_cast<uint64_t>(i), z1, z2);
+        const double s = S.stds[i];
+        const double x1 = s * z1, x2 = s * z2;
+        Up[2 * i] = S.contraction * U[2 * i] + S.beta * x1;
+        Up[2 * i + 1] = S.contraction * U[2 * i + 1] + S.beta * x2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double acc = 0.0;
+        for (int64_t i = 0; i < S.dim; ++i) {
+            const double r = Up[i] / S.stds[i >> 1];
+            acc += r * r;
+        }
+        S.norm_prop[b] = 0.5 * acc;
+    }
+}
+
+// velocity_from_coefficients -> tiled lattice block (images.h layout):
+// slot q of sample b = sp * u[ip] + sm * u[im] (indices -1 contribute 0).
+__global__ void pcn_pack_kernel(const int32_t* __restrict__ ip, const int32_t* __restrict__ im,
+                                const double* __restrict__ sp, const double* __restrict__ sm, int64_t stride,
+                                const double* __restrict__ Up, int64_t dim, double* __restrict__ blocks) {
+    const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t b = blockIdx.y;
+    if (q >= stride) return;
+    const double* u = Up + b * dim;
+    double v = 0.0;
+    const int32_t a = ip[q], c = im[q];
+    if (a >= 0) v = sp[q] * u[a];
+    if (c >= 0) v = v + sm[q] * u[c];
+    blocks[b * stride + q] = v;
+}
+
+// misfit (inference.cpp:98-103), the chain's uniform, the accept rule
+// (inference.cpp:154-165) and MAP tracking (inference.cpp:117-123).
+__global__ void pcn_accept_kernel(PcnStep S, const smc_estimate* __restrict__ est) {
+    const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (b >= S.n_chains) return;
+    double phi_prop = 0.0;
+    if (!S.noise_inf) {
+        double ss = 0.0;
+        for (int64_t j = 0; j < S.n_obs; ++j) {
+            const double r = S.data[j] - est[b * S.n_obs + j].mean;
+            ss += r * r;
+        }
+        phi_prop = ss / (2.0 * S.noise_std * S.noise_std);
+    }
+    bool accept = false;
+    if (S.init) {  // chain_init: the state is the proposal
+        accept = true;
+    } else {
+        const Uniform2 u = uniform_block(static_cast<uint32_t>(S.seeds[b]), static_cast<uint32_t>(S.seeds[b] >> 32),
+                                         kChainTag, 0u, S.ublk);
+        const double uacc = S.uhalf ? u.u1 : u.u0;
+        if (isfinite(phi_prop)) accept = uacc < exp(fmin(0.0, S.phi[b] - phi_prop));
+    }
+    if (accept) {
+        S.phi[b] = phi_prop;
+        S.norm_cur[b] = S.norm_prop[b];
+        if (!S.init) S.accepted[b] += 1;
+    }
+    S.acc_flag[b] = accept ? 1 : 0;
+    const double objective = S.phi[b] + S.norm_cur[b];
+    const bool better = S.init || objective < S.map_obj[b];
+    if (better) S.map_obj[b] = objective;
+    S.map_flag[b] = better ? 1 : 0;
+    if (!S.init && S.phi_trace) S.phi_trace[b * S.n_steps + S.step] = S.phi[b];
+}
+
+__global__ void pcn_commit_kernel(PcnStep S) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t b = blockIdx.y;
+    if (i >= S.dim) return;
+    double* U = S.U + b * S.dim;
+    if (S.acc_flag[b]) U[i] = S.Up[b * S.dim + i];
+    if (S.map_flag[b]) S.map_u[b * S.dim + i] = U[i];
+    if (S.sample_slot >= 0 && S.samples) S.samples[(b * S.n_samples + S.sample_slot) * S.dim + i] = U[i];
+}
+
+}  // namespace
+
+cudaError_t launch_pcn_propose(const PcnStep& S, cudaStream_t s) {
+    pcn_propose_kernel<<<static_cast<unsigned>(S.n_chains), 128, 0, s>>>(S);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pcn_pack(const int32_t* ip, const int32_t* im, const double* sp, const double* sm, int64_t stride,
+                            const double* Up, int64_t dim, int64_t n_chains, double* blocks, cudaStream_t s) {
+    const dim3 grid(static_cast<unsigned>((stride + 255) / 256), static_cast<unsigned>(n_chains));
+    pcn_pack_kernel<<<grid, 256, 0, s>>>(ip, im, sp, sm, stride, Up, dim, blocks);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pcn_accept(const PcnStep& S, const void* est, cudaStream_t s) {
+    pcn_accept_kernel<<<static_cast<unsigned>((S.n_chains + 127) / 128), 128, 0, s>>>(
+        S, static_cast<const smc_estimate*>(est));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pcn_commit(const PcnStep& S, cudaStream_t s) {
+    const dim3 grid(static_cast<unsigned>((S.dim + 255) / 256), static_cast<unsigned>(S.n_chains));
+    pcn_commit_kernel<<<grid, 256, 0, s>>>(S);
+    return cudaGetLastError();
+}
+
+}  // namespace smc

@@ -108,6 +108,17 @@ def main() -> None:
     g["misfit"] = {"u": hx(uk2), "data": data, "noise_std": 0.05, "forward_seed": 1234,
                    "phi": float(R.misfit(like, pk2, uk2, data, 0.05, 1234, 0)).hex()}
 
+    # run_chain (pCN, inference.cpp:170-194) on the sample_k2.json shape for
+    # three chain seeds, prior-drawn starts (the reference's own chain stream).
+    likespec = S.LikelihoodSpec(data=data, noise_std=0.05, forward=like, forward_seed=1234)
+    chains = []
+    for cseed in (31337, 7, 99):
+        r = R.run_chain(likespec, pk2, 40, 0.22, 5, 3, cseed)
+        chains.append({"seed": cseed, "phi_trace": hx(r["phi_trace"]), "samples": hx(r["samples"]),
+                       "final_u": hx(r["final_u"]), "map_u": hx(r["map_u"]), "final_phi": float(r["final_phi"]).hex(),
+                       "map_objective": float(r["map_objective"]).hex(), "accepted": r["accepted"]})
+    g["pcn"] = {"n_steps": 40, "beta": 0.22, "burn_in": 5, "thin": 3, "chains": chains}
+
     # Paper BVP (forward_bvp_box.json, seed 606, N_p 16000) — SURVEY §8c.
     bvp = specs.paper_bvp()
     vals, aux, failed, steps = R.bvp_particle_values(bvp, 0, 606, 256)

@@ -1,0 +1,62 @@
+"""Device-resident multi-chain pCN against the
+reference's run_chain (src/inference.cpp:170-194).
+
+Three chains run together (one batched forward map per step); chain c must
+reproduce the reference's run_chain with seed = seeds[c]: the same accepted
+count, Phi trace within the forward map's parity gate, and the same states.
+"""
+import numpy as np
+import pytest
+
+import paper_1808_10580_b200 as S
+import specs
+from conftest import unhex
+
+pytestmark = pytest.mark.gpu
+
+DATA = [-0.9065, -0.7528, -0.6665, -0.8091, -0.6508, -0.5135, -0.5185, -0.4553, -0.4066]
+
+
+def likelihood():
+    fwd = specs.c4_base(n_particles=160)
+    fwd.dt = 0.006
+    return S.LikelihoodSpec(data=DATA, noise_std=0.05, forward=fwd, forward_seed=1234)
+
+
+def test_chains_match_reference_run_chain(ctx, golden):
+    g = golden["pcn"]
+    prior = S.PriorSpec(2, 0.6, 2.5)
+    cfg = S.ChainConfig(n_steps=g["n_steps"], beta=g["beta"], burn_in=g["burn_in"], thin=g["thin"])
+    seeds = [c["seed"] for c in g["chains"]]
+    res = S.run_chains(cfg, prior, likelihood(), seeds, ctx=ctx)
+    for b, ref in enumerate(g["chains"]):
+        assert res["accepted"][b] == ref["accepted"]
+        trace = unhex(ref["phi_trace"])
+        assert np.allclose(res["phi_trace"][b], trace, rtol=1e-8, atol=1e-10)
+        assert np.allclose(res["final_u"][b], unhex(ref["final_u"]), rtol=0, atol=1e-12)
+        assert np.allclose(res["map_u"][b], unhex(ref["map_u"]), rtol=0, atol=1e-12)
+        assert abs(res["map_objective"][b] - float.fromhex(ref["map_objective"])) <= 1e-8 * abs(
+            float.fromhex(ref["map_objective"]))
+        samples = unhex(ref["samples"])
+        assert res["samples"][b].shape == samples.shape
+        assert np.allclose(res["samples"][b], samples, rtol=0, atol=1e-12)
+
+
+def test_chain_with_given_start_and_single_chain(ctx, golden):
+    prior = S.PriorSpec(2, 0.6, 2.5)
+    u0 = S.prior_draw(prior, 5, 0, 0, ctx)
+    cfg = S.ChainConfig(n_steps=10, beta=0.3, burn_in=0, thin=1)
+    one = S.run_chains(cfg, prior, likelihood(), [11], u0=u0[None, :], ctx=ctx)
+    two = S.run_chains(cfg, prior, likelihood(), [11, 12], u0=np.stack([u0, u0]), ctx=ctx)
+    # chains are independent of their batch neighbours
+    assert np.array_equal(one["phi_trace"][0], two["phi_trace"][0])
+    assert np.array_equal(one["final_u"][0], two["final_u"][0])
+    assert one["samples"].shape == (1, 10, prior.dimension())
+
+
+def test_chain_validation(ctx):
+    prior = S.PriorSpec(2, 0.6, 2.5)
+    with pytest.raises(ValueError, match="beta must be in"):
+        S.run_chains(S.ChainConfig(n_steps=3, beta=1.5), prior, likelihood(), [1], ctx=ctx)
+    with pytest.raises(ValueError, match="thin must be"):
+        S.run_chains(S.ChainConfig(n_steps=3, beta=0.1, thin=0), prior, likelihood(), [1], ctx=ctx)
