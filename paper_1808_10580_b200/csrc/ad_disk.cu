@@ -6,7 +6,8 @@
 // row's +/-j pairs unroll into 8 DFMAs on 4 coefficients, and every row folds
 // into v through P1[k1] = e^{2 pi i k1 x1}.  Coefficients are staged once per
 // block in shared memory and read with broadcast vector loads at compile-time
-// offsets, each load feeding all P particles of the thread.  Modes absent from
+// offsets, each load feeding all P particles of the thread.  One coefficient
+// block per parameter sample (blockIdx.z), disk_shape.h layout.  Modes absent from
 // the caller's field are zero coefficients; the host only picks this kernel
 // when the field fills most of its disk.
 #include <cuda_runtime.h>
@@ -21,11 +22,6 @@ namespace smc {
 namespace {
 
 constexpr int kBlock = 128;
-
-template <int K, class T>
-struct DiskCoef {
-    T c[DiskShape<K>::n_coef];
-};
 
 // Coefficients staged in shared memory, read with volatile vector loads at
 // compile-time offsets: one LDS.128 (broadcast) per two coefficients, kept
@@ -196,9 +192,12 @@ __device__ __forceinline__ void velocity_disk(const SmemCoef<T>& C, const T (&x1
 }
 
 template <int K, class T, int P>
-__global__ void __launch_bounds__(kBlock, (K <= 8 ? 4 : 3)) ad_particles_disk(const AdLaunch L, const DiskCoef<K, T> Pc) {
+__global__ void __launch_bounds__(kBlock, (K <= 8 ? 4 : 3)) ad_particles_disk(const AdLaunch L, const double* coef) {
+    // this sample's coefficient block -> shared memory (compute type)
     __shared__ __align__(16) T staged[DiskShape<K>::n_coef];
-    for (int i = threadIdx.x; i < DiskShape<K>::n_coef; i += kBlock) staged[i] = Pc.c[i];
+    const int sample = blockIdx.z;
+    const double* src = coef + static_cast<int64_t>(sample) * DiskShape<K>::n_coef;
+    for (int i = threadIdx.x; i < DiskShape<K>::n_coef; i += kBlock) staged[i] = T(src[i]);
     __syncthreads();
     const SmemCoef<T> C{static_cast<uint32_t>(__cvta_generic_to_shared(staged))};
     const int obs = blockIdx.y;
@@ -208,20 +207,19 @@ __global__ void __launch_bounds__(kBlock, (K <= 8 ? 4 : 3)) ad_particles_disk(co
     int64_t local[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) local[p] = base + static_cast<int64_t>(p) * kBlock;
-    ad_particles_p<T, P>(L, obs, 0, local, span,
+    ad_particles_p<T, P>(L, obs, sample, local, span,
                          [&](const T (&x1)[P], const T (&x2)[P], T (&v1)[P], T (&v2)[P]) {
                              velocity_disk<K, T, P>(C, x1, x2, v1, v2);
                          });
 }
 
 template <int K, class T, int P>
-cudaError_t launch_k(const AdLaunch& L, const double* host_coef, cudaStream_t s) {
-    DiskCoef<K, T> C;
-    for (int i = 0; i < DiskShape<K>::n_coef; ++i) C.c[i] = static_cast<T>(host_coef[i]);
+cudaError_t launch_k(const AdLaunch& L, const double* coef, cudaStream_t s) {
     const int64_t span = L.p_end - L.p_begin;
     const int64_t per_block = static_cast<int64_t>(kBlock) * P;
-    const dim3 grid(static_cast<unsigned>((span + per_block - 1) / per_block), static_cast<unsigned>(L.n_obs), 1);
-    ad_particles_disk<K, T, P><<<grid, kBlock, 0, s>>>(L, C);
+    const dim3 grid(static_cast<unsigned>((span + per_block - 1) / per_block), static_cast<unsigned>(L.n_obs),
+                    static_cast<unsigned>(L.n_samples));
+    ad_particles_disk<K, T, P><<<grid, kBlock, 0, s>>>(L, coef);
     return cudaGetLastError();
 }
 
@@ -255,10 +253,9 @@ cudaError_t dispatch(const AdLaunch& L, int K, const double* c, cudaStream_t s) 
 
 }  // namespace
 
-cudaError_t launch_ad_disk(const AdLaunch& L, int K, const double* host_coef, cudaStream_t s) {
+cudaError_t launch_ad_disk(const AdLaunch& L, int K, const double* coef, cudaStream_t s) {
     if (L.p_end - L.p_begin <= 0) return cudaSuccess;
-    if (L.n_samples != 1) return cudaErrorNotSupported;
-    return L.precision == 1 ? dispatch<float>(L, K, host_coef, s) : dispatch<double>(L, K, host_coef, s);
+    return L.precision == 1 ? dispatch<float>(L, K, coef, s) : dispatch<double>(L, K, coef, s);
 }
 
 }  // namespace smc

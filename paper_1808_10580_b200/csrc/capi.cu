@@ -239,8 +239,8 @@ VelImg patch(const VelRef& r, unsigned char* base) {
 // Everything a K1 launch needs, prepared and uploaded.
 struct AdPrepared {
     AdLaunch L{};
-    int disk_K = 0;            // > 0: use the compile-time disk kernel
-    std::vector<double> disk;  // its coefficient block
+    int disk_K = 0;                  // > 0: use the compile-time disk kernel
+    const double* disk = nullptr;    // its coefficient blocks (device, one per sample)
     int64_t n_obs = 0;
     int64_t steps_per_particle_sum = 0;  // sum_j n_j
 };
@@ -265,7 +265,22 @@ AdPrepared prepare_ad(smc_ctx* ctx, const smc_ad_problem& p, const std::vector<c
     const size_t obs_off = im.add_vec(obs);
     const ScalarRef th = add_scalar(im, p.initial_condition);
     const VelRef vr = add_velocity(im, structure, fills);
+    // Dense fields with K <= kDiskMaxK take the compile-time disk kernel.
+    size_t disk_off = 0;
+    const bool disk = !structure.is_constant && p.precision != SMC_FP64_STRICT && structure.K <= kDiskMaxK &&
+                      2 * structure.modes.size() >= static_cast<size_t>(disk_n_modes(structure.K)) &&
+                      std::getenv("SMC_DISABLE_DISK") == nullptr;
+    if (disk) {
+        const size_t nc = static_cast<size_t>(disk_n_coef(structure.K));
+        disk_off = im.reserve(nc * fills.size() * sizeof(double));
+        for (size_t b = 0; b < fills.size(); ++b)
+            disk_fill(structure.K, *fills[b], reinterpret_cast<double*>(im.bytes.data() + disk_off) + b * nc);
+    }
     unsigned char* base = ctx->upload(im);
+    if (disk) {
+        out.disk_K = structure.K;
+        out.disk = reinterpret_cast<const double*>(base + disk_off);
+    }
     AdLaunch& L = out.L;
     L.vel = patch(vr, base);
     L.theta0 = patch(th, base);
@@ -279,20 +294,12 @@ AdPrepared prepare_ad(smc_ctx* ctx, const smc_ad_problem& p, const std::vector<c
     L.precision = p.precision;
     L.sigma = sigma;
     out.n_obs = obs_count;
-    // Dense fields with K <= kDiskMaxK take the compile-time disk kernel.
-    if (!structure.is_constant && fills.size() == 1 && p.precision != SMC_FP64_STRICT && structure.K <= kDiskMaxK &&
-        2 * structure.modes.size() >= static_cast<size_t>(disk_n_modes(structure.K)) &&
-        std::getenv("SMC_DISABLE_DISK") == nullptr) {
-        out.disk_K = structure.K;
-        out.disk.resize(static_cast<size_t>(disk_n_coef(structure.K)));
-        disk_fill(structure.K, *fills[0], out.disk.data());
-    }
     return out;
 }
 
-void run_particles(smc_ctx* ctx, AdLaunch& L, const AdPrepared* P = nullptr) {
-    if (P && P->disk_K > 0 && L.n_samples == 1) {
-        CK(launch_ad_disk(L, P->disk_K, P->disk.data(), ctx->stream));
+void run_particles(smc_ctx* ctx, AdLaunch& L, const AdPrepared* P = nullptr, int64_t sample0 = 0) {
+    if (P && P->disk_K > 0) {
+        CK(launch_ad_disk(L, P->disk_K, P->disk + sample0 * disk_n_coef(P->disk_K), ctx->stream));
     } else if (L.precision == SMC_FP64_STRICT) {
         if (L.n_samples != 1) raise(SMC_EINVAL, "strict precision is single-sample only");
         if (!L.vel.is_constant && L.vel.K > 128) raise(SMC_EINVAL, "strict precision supports max_wavenumber <= 128");
@@ -615,7 +622,7 @@ smc_status smc_ad_observe_batched(smc_ctx* ctx, const smc_ad_problem* base, cons
             L.n_samples = static_cast<int32_t>(nb);
             if (!L.vel.is_constant) L.vel.lat.coef += b0 * L.vel.lat.sample_stride;
             L.values = values + b0 * n_obs * n;
-            run_particles(ctx, L);
+            run_particles(ctx, L, &P, b0);
         }
         CK(cudaEventRecord(ctx->ev[1], ctx->stream));
         reduce_ad(ctx, values, n, n_samples * n_obs, out);
@@ -816,8 +823,11 @@ smc_status smc_pcn_chains(smc_ctx* ctx, const smc_ad_problem* forward, const smc
         std::sort(structure.modes.begin(), structure.modes.end(), [](const HostMode& a, const HostMode& b) {
             return a.k1 != b.k1 ? a.k1 < b.k1 : a.k2 < b.k2;
         });
+        // u -> coefficient-block gather map, in the disk layout (disk_shape.h,
+        // K <= kDiskMaxK) or the tiled lattice layout (images.h)
+        const bool use_disk = prior->cutoff <= kDiskMaxK && std::getenv("SMC_DISABLE_DISK") == nullptr;
         const LatticeHost Lh = lattice_structure(structure);
-        const int64_t stride = Lh.stride;
+        const int64_t stride = use_disk ? disk_n_coef(prior->cutoff) : Lh.stride;
         std::vector<int32_t> ip(static_cast<size_t>(stride), -1), imv(static_cast<size_t>(stride), -1);
         std::vector<double> sp(static_cast<size_t>(stride), 0.0), sm(static_cast<size_t>(stride), 0.0);
         {
@@ -836,26 +846,43 @@ smc_status smc_pcn_chains(smc_ctx* ctx, const smc_ad_problem* forward, const smc
                     sm[slot] = msign * g(k1m, k2m);
                 }
             };
-            for (int t = 0; t < Lh.n_tiles; ++t) {
-                const int2 tl = Lh.tiles[static_cast<size_t>(t)];
-                for (int k1 = 1; k1 <= tl.x; ++k1)
-                    for (int q = 0; q < kLatticeTileHost; ++q) {
-                        const int j = kLatticeTileHost * t + q + 1;
-                        if (j > K) break;
-                        const int64_t base = tl.y + static_cast<int64_t>(k1 - 1) * kLatticeTileHost * 4 + 4 * q;
-                        set(base + 0, k1, j, k1, -j, 0, 1.0);   // alpha_re
-                        set(base + 1, k1, j, k1, -j, 1, 1.0);   // alpha_im
-                        set(base + 2, k1, j, k1, -j, 0, -1.0);  // beta_re
-                        set(base + 3, k1, j, k1, -j, 1, -1.0);  // beta_im
-                    }
-            }
-            for (int j = 1; j <= Lh.J0; ++j) {
-                set(Lh.row0_off + 2 * (j - 1), 0, j, -1, 0, 0, 0.0);
-                set(Lh.row0_off + 2 * (j - 1) + 1, 0, j, -1, 0, 1, 0.0);
-            }
-            for (int k1 = 1; k1 <= Lh.R; ++k1) {
-                set(Lh.g0_off + 2 * k1, k1, 0, -1, 0, 0, 0.0);
-                set(Lh.g0_off + 2 * k1 + 1, k1, 0, -1, 0, 1, 0.0);
+            auto pair = [&](int64_t base, int k1, int j) {
+                set(base + 0, k1, j, k1, -j, 0, 1.0);   // alpha_re
+                set(base + 1, k1, j, k1, -j, 1, 1.0);   // alpha_im
+                set(base + 2, k1, j, k1, -j, 0, -1.0);  // beta_re
+                set(base + 3, k1, j, k1, -j, 1, -1.0);  // beta_im
+            };
+            if (use_disk) {
+                int64_t pidx = 0;
+                for (int k1 = 1; k1 <= K; ++k1)
+                    for (int j = 1; j <= disk_jmax(K, k1); ++j, ++pidx) pair(4 * pidx, k1, j);
+                const int64_t row0 = 4 * disk_n_pairs(K), g0 = row0 + 2 * K;
+                for (int j = 1; j <= K; ++j) {
+                    set(row0 + 2 * (j - 1), 0, j, -1, 0, 0, 0.0);
+                    set(row0 + 2 * (j - 1) + 1, 0, j, -1, 0, 1, 0.0);
+                }
+                for (int k1 = 1; k1 <= K; ++k1) {
+                    set(g0 + 2 * (k1 - 1), k1, 0, -1, 0, 0, 0.0);
+                    set(g0 + 2 * (k1 - 1) + 1, k1, 0, -1, 0, 1, 0.0);
+                }
+            } else {
+                for (int t = 0; t < Lh.n_tiles; ++t) {
+                    const int2 tl = Lh.tiles[static_cast<size_t>(t)];
+                    for (int k1 = 1; k1 <= tl.x; ++k1)
+                        for (int q = 0; q < kLatticeTileHost; ++q) {
+                            const int j = kLatticeTileHost * t + q + 1;
+                            if (j > K) break;
+                            pair(tl.y + static_cast<int64_t>(k1 - 1) * kLatticeTileHost * 4 + 4 * q, k1, j);
+                        }
+                }
+                for (int j = 1; j <= Lh.J0; ++j) {
+                    set(Lh.row0_off + 2 * (j - 1), 0, j, -1, 0, 0, 0.0);
+                    set(Lh.row0_off + 2 * (j - 1) + 1, 0, j, -1, 0, 1, 0.0);
+                }
+                for (int k1 = 1; k1 <= Lh.R; ++k1) {
+                    set(Lh.g0_off + 2 * k1, k1, 0, -1, 0, 0, 0.0);
+                    set(Lh.g0_off + 2 * k1 + 1, k1, 0, -1, 0, 1, 0.0);
+                }
             }
         }
         if (static_cast<int64_t>(p.n_obs) <= 0) raise(SMC_EINVAL, "AdProblemSpec: no observations");
@@ -928,8 +955,10 @@ smc_status smc_pcn_chains(smc_ctx* ctx, const smc_ad_problem* forward, const smc
         AdPrepared P = prepare_ad(ctx, p, {&structure}, structure, 0, n_obs);
         P.L.seed = forward_seed;
         P.L.seeds = nullptr;
-        P.L.vel.lat.coef = d_blocks;
-        P.L.vel.lat.sample_stride = stride;
+        if (!use_disk) {
+            P.L.vel.lat.coef = d_blocks;
+            P.L.vel.lat.sample_stride = stride;
+        }
         double* values = ctx->values.get<double>(static_cast<size_t>(B * n_obs * n));
 
         auto forward_map = [&]() -> smc_estimate* {
@@ -938,9 +967,13 @@ smc_status smc_pcn_chains(smc_ctx* ctx, const smc_ad_problem* forward, const smc
             for (int64_t b0 = 0; b0 < B; b0 += kMaxZ) {
                 AdLaunch L = P.L;
                 L.n_samples = static_cast<int32_t>(std::min(kMaxZ, B - b0));
-                L.vel.lat.coef = d_blocks + b0 * stride;
                 L.values = values + b0 * n_obs * n;
-                run_particles(ctx, L);
+                if (use_disk) {
+                    CK(launch_ad_disk(L, prior->cutoff, d_blocks + b0 * stride, s));
+                } else {
+                    L.vel.lat.coef = d_blocks + b0 * stride;
+                    run_particles(ctx, L);
+                }
             }
             count_launches(ctx, 1);
             return reduce_ad_device(ctx, values, n, B * n_obs);

@@ -38,10 +38,9 @@ cudaError_t launch_ad_particles_fp32(const AdLaunch& L, cudaStream_t s);
 cudaError_t launch_ad_particles_strict(const AdLaunch& L, cudaStream_t s);
 
 // K1 specialised for the full disk |k| <= K (K <= kDiskMaxK, disk_shape.h):
-// the coefficient block (disk_n_coef(K) doubles, host memory) travels as a
-// kernel parameter.  Returns cudaErrorNotSupported when K has no
-// specialisation.  Single coefficient set (n_samples == 1).
-cudaError_t launch_ad_disk(const AdLaunch& L, int K, const double* host_coef, cudaStream_t s);
+// coef = device blocks of disk_n_coef(K) doubles, one per sample.  Returns
+// cudaErrorNotSupported when K has no specialisation.
+cudaError_t launch_ad_disk(const AdLaunch& L, int K, const double* coef, cudaStream_t s);
 
 // K2: Dirichlet exit-time walkers (Algorithm 2, PAPER.md:162-178;
 // sde.cpp:52-77 + forward_bvp.cpp:39-46).  Persistent warps: a lane whose

@@ -46,6 +46,27 @@ if args.config == "c4":
           f"{st.particle_steps / st.particle_kernel_ms * 1e3:.4g} particle-steps/s; "
           f"{14 * 980 + 12 * 24 + 20} flop/step -> {(14 * 980 + 12 * 24 + 20) * st.particle_steps / st.particle_kernel_ms / 1e9:.2f} TFLOP/s")
     sys.exit(0)
+if args.config in ("pcn", "pcn8"):
+    # sample_k2.json shape (K=2) or the paper's Ex. 2 size (K=8, N_u=197): B chains
+    import time
+    import numpy as np
+    import specs
+    B = args.particles or 100
+    prior = S.PriorSpec(2, 0.6, 2.5) if args.config == "pcn" else S.PriorSpec(8, 0.6, 2.5)
+    fwd = specs.c4_base(n_particles=160)
+    fwd.dt = 0.006
+    like = S.LikelihoodSpec(data=[-0.9065, -0.7528, -0.6665, -0.8091, -0.6508, -0.5135, -0.5185, -0.4553, -0.4066],
+                            noise_std=0.05, forward=fwd, forward_seed=1234)
+    n_steps = int(os.environ.get('PCN_STEPS', '2000'))
+    cfg = S.ChainConfig(n_steps=n_steps, beta=0.22, burn_in=min(200, n_steps // 2), thin=10)
+    S.run_chains(S.ChainConfig(n_steps=5, beta=0.22), prior, like, list(range(B)), ctx=ctx)  # warm-up
+    t0 = time.perf_counter()
+    res = S.run_chains(cfg, prior, like, list(range(B)), ctx=ctx)
+    el = time.perf_counter() - t0
+    print(f"{args.config} B={B} dim={prior.dimension()}: {n_steps} steps in {el:.3f} s -> "
+          f"{B * n_steps / el:.4g} chain-steps/s ({el / n_steps * 1e6:.1f} us/step), "
+          f"acceptance {res['acceptance_rate'].mean():.3f}")
+    sys.exit(0)
 if args.config in ("c3", "c3b"):
     # paper BVP, F=(1,-0.5,2), 25 obs, 1e6 walkers/obs, seed 606
     import specs
