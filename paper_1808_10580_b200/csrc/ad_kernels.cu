@@ -17,11 +17,12 @@
 namespace smc {
 namespace {
 
-constexpr int kBlock = 256;
-constexpr size_t kSmemLimit = 64 * 1024;
+constexpr size_t kSmemLimit = 64 * 1024;   // tables up to here: 256-thread blocks, 2 per SM
+constexpr size_t kSmemMax = 220 * 1024;    // larger tables: one 512-thread block per SM
+constexpr size_t kSmemHard = 227 * 1024;
 
-template <class T, bool SMEM>
-__global__ void __launch_bounds__(kBlock, 2) ad_particles(const AdLaunch L) {
+template <class T, bool SMEM, int kBlock>
+__global__ void __launch_bounds__(kBlock, 512 / kBlock) ad_particles(const AdLaunch L) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int obs = blockIdx.y;
     const int sample = blockIdx.z;
@@ -51,25 +52,29 @@ __global__ void __launch_bounds__(kBlock, 2) ad_particles(const AdLaunch L) {
     });
 }
 
+template <class T, bool SMEM, int BS>
+void go(const AdLaunch& L, int64_t span, size_t smem, cudaStream_t s) {
+    const dim3 grid(static_cast<unsigned>((span + BS - 1) / BS), static_cast<unsigned>(L.n_obs),
+                    static_cast<unsigned>(L.n_samples));
+    if constexpr (SMEM) {
+        static bool configured = false;
+        if (!configured) {
+            cudaFuncSetAttribute(ad_particles<T, true, BS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(kSmemHard));
+            configured = true;
+        }
+    }
+    ad_particles<T, SMEM, BS><<<grid, BS, smem, s>>>(L);
+}
+
 template <class T>
 cudaError_t launch(const AdLaunch& L, cudaStream_t s) {
     const int64_t span = L.p_end - L.p_begin;
     if (span <= 0) return cudaSuccess;
-    const dim3 grid(static_cast<unsigned>((span + kBlock - 1) / kBlock), static_cast<unsigned>(L.n_obs),
-                    static_cast<unsigned>(L.n_samples));
     const size_t smem = L.vel.is_constant ? 0 : static_cast<size_t>(L.vel.lat.sample_stride) * sizeof(T);
-    const bool use_smem = smem <= kSmemLimit && std::getenv("SMC_LATTICE_GLOBAL") == nullptr;
-    if (use_smem) {
-        static bool configured = false;
-        if (!configured) {
-            cudaFuncSetAttribute(ad_particles<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(kSmemLimit));
-            configured = true;
-        }
-        ad_particles<T, true><<<grid, kBlock, smem, s>>>(L);
-    } else {
-        ad_particles<T, false><<<grid, kBlock, 0, s>>>(L);
-    }
+    if (std::getenv("SMC_LATTICE_GLOBAL") != nullptr || smem > kSmemMax) go<T, false, 256>(L, span, 0, s);
+    else if (smem <= kSmemLimit) go<T, true, 256>(L, span, smem, s);
+    else go<T, true, 512>(L, span, smem, s);
     return cudaGetLastError();
 }
 
