@@ -195,6 +195,19 @@ smc_status smc_bvp_observe(smc_ctx* ctx, const smc_bvp_problem* prob, uint64_t s
 smc_status smc_bvp_observe_range(smc_ctx* ctx, const smc_bvp_problem* prob, uint64_t seed, int64_t obs_begin,
                                  int64_t obs_count, smc_estimate* out);
 
+/* Forcing basis of the Dirichlet map.  With common
+ * random numbers the walker paths do not depend on the forcing amplitudes F,
+ * so for a Gaussian-bump forcing (1..4 bumps; the amplitudes in `prob` are
+ * ignored) one pass yields, per observation j,
+ *   mean_bc[j]            = E[theta_bc(X_tau)]
+ *   mean_basis[j][k]      = E[int_0^tau phi_k(X_t) dt],  phi_k = exp(-a |x - c_k|^2)
+ * and observe_bvp's mean for any F is mean_bc[j] - sum_k F_k mean_basis[j][k]
+ * (forward_bvp.cpp:45 by linearity) — what forcing_cost (optimize.cpp:161-173)
+ * evaluates at every Nelder-Mead vertex.  mean_tau / n_failed as
+ * observe_bvp's aux_mean / n_failed.  Any output may be NULL. */
+smc_status smc_bvp_forcing_basis(smc_ctx* ctx, const smc_bvp_problem* prob, uint64_t seed, double* mean_bc,
+                                 double* mean_basis, double* mean_tau, int64_t* n_failed);
+
 /* ---- device-resident multi-chain pCN ------------
  * run_chain (include/scalarmc/inference.hpp:95-99, src/inference.cpp:170-194)
  * for n_chains independent chains at once: every step evaluates all chains'

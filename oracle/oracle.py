@@ -253,6 +253,23 @@ class Reference(_Checker):
         return {"phi_trace": trace[:n_steps], "samples": samples[:n_samples], "final_u": final_u, "map_u": map_u,
                 "final_phi": sc[0], "map_objective": sc[1], "accepted": int(sc[2])}
 
+    def optimize_forcing(self, spec, initial, centers, sharpness, target, x_tol, f_tol, max_iter, initial_step,
+                         seed: int, workers: int = 0) -> dict:
+        p, keep = spec._pod()
+        ini = np.ascontiguousarray(initial, dtype=np.float64)
+        c = np.ascontiguousarray(centers, dtype=np.float64).reshape(-1, 2)
+        t = np.ascontiguousarray(target, dtype=np.float64)
+        arg = np.zeros(ini.size)
+        sc = np.zeros(2)
+        reason = C.create_string_buffer(16)
+        rc = self.lib.ref_optimize_forcing(C.byref(p), C.c_int64(ini.size), ini.ctypes.data_as(_dp),
+                                           c.ctypes.data_as(_dp), C.c_double(sharpness), t.ctypes.data_as(_dp),
+                                           C.c_double(x_tol), C.c_double(f_tol), C.c_int(max_iter),
+                                           C.c_double(initial_step), C.c_uint64(seed), C.c_int(workers),
+                                           arg.ctypes.data_as(_dp), sc.ctypes.data_as(_dp), reason)
+        _status(self.lib, self.prefix, rc)
+        return {"argmin": arg, "min_value": sc[0], "iterations": int(sc[1]), "stop_reason": reason.value.decode()}
+
     def resolved_dt_ad(self, spec) -> float:
         p, keep = spec._pod()
         out = C.c_double()

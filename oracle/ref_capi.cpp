@@ -12,6 +12,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <exception>
 #include <optional>
@@ -350,6 +351,35 @@ int ref_run_chain(const smc_ad_problem* base, const smc_prior* prior, const doub
         scalars[0] = r.final_state.phi;
         scalars[1] = r.map_objective;
         scalars[2] = static_cast<double>(r.final_state.accepted);
+    });
+}
+
+// optimize_forcing (optimize.cpp:175-185), unchanged reference code.
+// out: argmin [n_bumps], scalars = (min_value, iterations); reason: >= 16 chars.
+int ref_optimize_forcing(const smc_bvp_problem* base, int64_t n_bumps, const double* initial, const double* centers,
+                         double sharpness, const double* target, double x_tol, double f_tol, int max_iter,
+                         double initial_step, uint64_t seed, int workers, double* argmin, double* scalars,
+                         char* reason) {
+    return guarded([&] {
+        ForcingControl c;
+        for (int64_t j = 0; j < n_bumps; ++j) {
+            c.initial_amplitudes.push_back(initial[j]);
+            c.centers.push_back({centers[2 * j], centers[2 * j + 1]});
+        }
+        c.sharpness = sharpness;
+        const BvpProblemSpec b = to_bvp(*base);
+        c.observation_points = b.observations;
+        c.target.assign(target, target + base->n_obs);
+        NelderMeadOptions o;
+        o.x_tol = x_tol;
+        o.f_tol = f_tol;
+        o.max_iter = max_iter;
+        o.initial_step = initial_step;
+        const NelderMeadResult r = optimize_forcing(c, b, o, seed, workers);
+        for (int64_t j = 0; j < n_bumps; ++j) argmin[j] = r.argmin[static_cast<std::size_t>(j)];
+        scalars[0] = r.min_value;
+        scalars[1] = r.iterations;
+        std::snprintf(reason, 16, "%s", r.stop_reason.c_str());
     });
 }
 

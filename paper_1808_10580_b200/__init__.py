@@ -15,9 +15,11 @@ from .api import (  # noqa: F401
     DiffusionModel,
     Domain,
     ESTIMATE_DTYPE,
+    ForcingBasis,
     ForcingControl,
     FourierVelocityField,
     LikelihoodSpec,
+    NelderMeadOptions,
     ParticleEstimate,
     Point2,
     Precision,
@@ -30,7 +32,10 @@ from .api import (  # noqa: F401
     ad_particle_values,
     bvp_particle_values,
     default_context,
+    forcing_basis,
     forcing_cost,
+    nelder_mead,
+    optimize_forcing,
     normal_pairs_device,
     observe_ad,
     observe_ad_batched,

@@ -114,6 +114,8 @@ _PROTOS = {
                                   C.POINTER(smc_estimate)]),
     "smc_bvp_observe_range": (C.c_int, [C.c_void_p, C.POINTER(smc_bvp_problem), C.c_uint64, C.c_int64,
                                         C.c_int64, C.POINTER(smc_estimate)]),
+    "smc_bvp_forcing_basis": (C.c_int, [C.c_void_p, C.POINTER(smc_bvp_problem), C.c_uint64, _dp, _dp, _dp,
+                                        C.POINTER(C.c_int64)]),
     "smc_pcn_num_samples": (C.c_int64, [C.POINTER(smc_chain_config)]),
     "smc_pcn_chains": (C.c_int, [C.c_void_p, C.POINTER(smc_ad_problem), C.POINTER(smc_prior), _dp, C.c_double,
                                  C.c_uint64, C.c_int64, C.POINTER(C.c_uint64), _dp, C.POINTER(smc_chain_config),

@@ -48,6 +48,14 @@ struct Forcing {
             }
         }
     }
+    // the unit-amplitude bumps phi_j(x) = exp(-a |x - c_j|^2) (forcing basis)
+    __device__ __forceinline__ void basis(double x1, double x2, double (&phi)[NB > 0 ? NB : 1]) const {
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            const double d1 = x1 - c1[i], d2 = x2 - c2[i];
+            phi[i] = SMC_SCALAR_EXP(neg_a * (d1 * d1 + d2 * d2));
+        }
+    }
     __device__ __forceinline__ double operator()(const ScalarImg& f, double x1, double x2) const {
         if constexpr (NB == 0) {
             return scalar_eval(f, x1, x2);
@@ -65,7 +73,11 @@ struct Forcing {
 
 // VEL: 0 = runtime dispatch (constant or Fourier), 1 = constant velocity
 // only (the lattice series is compiled out, which frees registers).
-template <class T, bool STRICT, int KCAP, int NB = 0, int VEL = 0>
+// BASIS (NB > 0, FP64): instead of one forcing integral, accumulate the NB
+// unit-bump integrals I_j = int phi_j(X_t) dt and store value = bc(X_tau), so
+// G(F) = E[bc] - sum_j F_j E[I_j] for every amplitude vector F from one pass
+// (common random numbers: the paths do not depend on F).
+template <class T, bool STRICT, int KCAP, int NB = 0, int VEL = 0, bool BASIS = false>
 __global__ void __launch_bounds__(kBvpBlock) bvp_walkers(const BvpLaunch L) {
     constexpr unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
@@ -79,6 +91,7 @@ __global__ void __launch_bounds__(kBvpBlock) bvp_walkers(const BvpLaunch L) {
     uint32_t obs = 0, particle = 0;
     int64_t step = 0;
     T x1 = T(0), x2 = T(0), f_int = T(0);
+    double I[NB > 0 ? NB : 1];
     unsigned long long my_steps = 0;
     cd p1[STRICT ? KCAP + 1 : 1], p2[STRICT ? KCAP + 1 : 1];
     const Forcing<NB> forcing(L.forcing);
@@ -101,6 +114,10 @@ __global__ void __launch_bounds__(kBvpBlock) bvp_walkers(const BvpLaunch L) {
                         x1 = T(__ldg(L.obs_x + 2 * obs));
                         x2 = T(__ldg(L.obs_x + 2 * obs + 1));
                         f_int = T(0);
+                        if constexpr (BASIS) {
+#pragma unroll
+                            for (int q = 0; q < NB; ++q) I[q] = 0.0;
+                        }
                         step = 0;
                         active = true;
                     }
@@ -138,19 +155,34 @@ __global__ void __launch_bounds__(kBvpBlock) bvp_walkers(const BvpLaunch L) {
                 n1 = fma(sr, xi1, fma(-v1, dt, x1));
                 n2 = fma(sr, xi2, fma(-v2, dt, x2));
             }
-            const T f = T(forcing(L.forcing, double(x1), double(x2)));
+            T f = T(0);
+            double phi[NB > 0 ? NB : 1];
+            if constexpr (BASIS) forcing.basis(double(x1), double(x2), phi);
+            else f = T(forcing(L.forcing, double(x1), double(x2)));
             ++my_steps;
             if (!domain_contains<T>(L.domain, n1, n2)) {
                 T h1, h2;
                 const T frac = boundary_exit<T>(L.domain, x1, x2, n1, n2, h1, h2);
-                f_int += f * frac * dt;
                 const T tau = T(double(step)) * dt + frac * dt;
-                L.values[w] = scalar_eval(L.boundary, double(h1), double(h2)) - double(f_int);
+                if constexpr (BASIS) {
+                    const unsigned long long nw = total;
+#pragma unroll
+                    for (int q = 0; q < NB; ++q) L.basis[q * nw + w] = I[q] + phi[q] * double(frac) * double(dt);
+                    L.values[w] = scalar_eval(L.boundary, double(h1), double(h2));
+                } else {
+                    f_int += f * frac * dt;
+                    L.values[w] = scalar_eval(L.boundary, double(h1), double(h2)) - double(f_int);
+                }
                 L.aux[w] = double(tau);
                 L.failed[w] = 0;
                 active = false;
             } else {
-                f_int += f * dt;
+                if constexpr (BASIS) {
+#pragma unroll
+                    for (int q = 0; q < NB; ++q) I[q] += phi[q] * double(dt);
+                } else {
+                    f_int += f * dt;
+                }
                 x1 = n1;
                 x2 = n2;
                 ++step;
@@ -158,6 +190,10 @@ __global__ void __launch_bounds__(kBvpBlock) bvp_walkers(const BvpLaunch L) {
                     L.values[w] = 0.0;
                     L.aux[w] = 0.0;
                     L.failed[w] = 1;
+                    if constexpr (BASIS) {
+#pragma unroll
+                        for (int q = 0; q < NB; ++q) L.basis[q * total + w] = 0.0;
+                    }
                     active = false;
                 }
             }

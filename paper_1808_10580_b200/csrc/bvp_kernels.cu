@@ -42,4 +42,24 @@ cudaError_t launch_bvp_walkers(const BvpLaunch& L, int n_sms, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+cudaError_t launch_bvp_basis(const BvpLaunch& L, int n_sms, cudaStream_t s) {
+    const unsigned long long total = static_cast<unsigned long long>(L.n_obs) * L.n_particles;
+    unsigned blocks = static_cast<unsigned>(n_sms) * 8u;
+    const unsigned long long need = (total + kBvpBlock - 1) / kBvpBlock;
+    if (need < blocks) blocks = static_cast<unsigned>(need > 0 ? need : 1);
+    const bool cv = L.vel.is_constant;
+    switch (L.forcing.n) {
+        case 1: cv ? bvp_walkers<double, false, 0, 1, 1, true><<<blocks, kBvpBlock, 0, s>>>(L)
+                   : bvp_walkers<double, false, 0, 1, 0, true><<<blocks, kBvpBlock, 0, s>>>(L); break;
+        case 2: cv ? bvp_walkers<double, false, 0, 2, 1, true><<<blocks, kBvpBlock, 0, s>>>(L)
+                   : bvp_walkers<double, false, 0, 2, 0, true><<<blocks, kBvpBlock, 0, s>>>(L); break;
+        case 3: cv ? bvp_walkers<double, false, 0, 3, 1, true><<<blocks, kBvpBlock, 0, s>>>(L)
+                   : bvp_walkers<double, false, 0, 3, 0, true><<<blocks, kBvpBlock, 0, s>>>(L); break;
+        case 4: cv ? bvp_walkers<double, false, 0, 4, 1, true><<<blocks, kBvpBlock, 0, s>>>(L)
+                   : bvp_walkers<double, false, 0, 4, 0, true><<<blocks, kBvpBlock, 0, s>>>(L); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
 }  // namespace smc

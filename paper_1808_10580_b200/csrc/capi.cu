@@ -1092,6 +1092,75 @@ smc_status smc_bvp_observe_range(smc_ctx* ctx, const smc_bvp_problem* p, uint64_
     });
 }
 
+smc_status smc_bvp_forcing_basis(smc_ctx* ctx, const smc_bvp_problem* p, uint64_t seed, double* mean_bc,
+                                 double* mean_basis, double* mean_tau, int64_t* n_failed) {
+    return guarded([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (p->forcing.kind != SMC_SCALAR_BUMPS || p->forcing.n_terms < 1 || p->forcing.n_terms > 4)
+            raise(SMC_EINVAL, "bvp_forcing_basis: forcing must be a sum of 1..4 Gaussian bumps");
+        if (p->precision != SMC_FP64) raise(SMC_EINVAL, "bvp_forcing_basis: FP64 only");
+        ctx->stats = smc_stats{};
+        BvpLaunch L = prepare_bvp(ctx, *p, 0, p->n_obs);
+        L.seed = seed;
+        const int64_t n = p->n_particles, n_obs = p->n_obs, nb = p->forcing.n_terms;
+        cudaStream_t s = ctx->stream;
+        const size_t total = static_cast<size_t>(n_obs * n);
+        L.values = ctx->values.get<double>(total);
+        L.aux = ctx->aux.get<double>(total);
+        L.failed = ctx->flags.get<uint8_t>(total);
+        L.basis = ctx->tmp_c.get<double>(total * static_cast<size_t>(nb));
+        unsigned long long* ctr = ctx->flags2.get<unsigned long long>(2);
+        CK(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), s));
+        L.counter = ctr;
+        L.step_total = ctr + 1;
+        int sms = 0;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+        CK(cudaEventRecord(ctx->ev[0], s));
+        CK(launch_bvp_basis(L, sms, s));
+        CK(cudaEventRecord(ctx->ev[1], s));
+        count_launches(ctx, 1);
+        // per quantity: compact valid walkers (executor.cpp:93-101), tree sum, / n_valid
+        const int64_t chunks = smc_num_chunks(n);
+        double* cvals = ctx->tmp_a.get<double>(total);
+        double* caux = ctx->tmp_b.get<double>(total);
+        DevBuf ctmp;
+        int64_t* chunk_tmp = ctmp.get<int64_t>(static_cast<size_t>(2 * n_obs * chunks));
+        int64_t* counts = ctx->counts.get<int64_t>(static_cast<size_t>(n_obs));
+        double* scratch = ctx->scratch.get<double>(static_cast<size_t>(2 * n_obs * std::max<int64_t>(chunks, 1)));
+        double* sums = ctx->sums.get<double>(static_cast<size_t>(n_obs * (nb + 2)));
+        double* means = ctx->means.get<double>(static_cast<size_t>(n_obs * (nb + 2)));
+        int launches = 0;
+        // values + exit times
+        CK(compact_valid(L.values, L.aux, L.failed, n, n_obs, cvals, caux, counts, chunk_tmp, s));
+        CK(tree_reduce(cvals, n, counts, n, n_obs, sums, nullptr, 0, scratch, s, &launches));
+        CK(tree_reduce(caux, n, counts, n, n_obs, sums + n_obs, nullptr, 0, scratch, s, &launches));
+        for (int64_t q = 0; q < nb; ++q) {
+            const double* bq = L.basis + q * static_cast<int64_t>(total);
+            CK(compact_valid(bq, bq, L.failed, n, n_obs, cvals, caux, counts, chunk_tmp, s));
+            CK(tree_reduce(cvals, n, counts, n, n_obs, sums + (2 + q) * n_obs, nullptr, 0, scratch, s, &launches));
+        }
+        for (int64_t q = 0; q < nb + 2; ++q)
+            CK(launch_divide(sums + q * n_obs, counts, n, n_obs, means + q * n_obs, s));
+        count_launches(ctx, launches + 3 * (nb + 1) + nb + 2);
+        std::vector<double> h(static_cast<size_t>(n_obs * (nb + 2)));
+        std::vector<int64_t> hc(static_cast<size_t>(n_obs));
+        CK(cudaMemcpyAsync(h.data(), means, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(hc.data(), counts, sizeof(int64_t) * n_obs, cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(ctx->ev[2], s));
+        CK(cudaStreamSynchronize(s));
+        ctmp.release();
+        finish_stats(ctx);
+        for (int64_t j = 0; j < n_obs; ++j) {
+            if (hc[static_cast<size_t>(j)] == 0) raise(SMC_ERUNTIME, "map_reduce: every particle of an observation failed");
+            if (mean_bc) mean_bc[j] = h[static_cast<size_t>(j)];
+            if (mean_tau) mean_tau[j] = h[static_cast<size_t>(n_obs + j)];
+            if (n_failed) n_failed[j] = n - hc[static_cast<size_t>(j)];
+            for (int64_t q = 0; q < nb; ++q)
+                if (mean_basis) mean_basis[j * nb + q] = h[static_cast<size_t>((2 + q) * n_obs + j)];
+        }
+    });
+}
+
 smc_status smc_bvp_particle_values(smc_ctx* ctx, const smc_bvp_problem* p, uint64_t obs_index, uint64_t seed,
                                    int64_t n, double* values, double* aux, uint8_t* failed) {
     return guarded([&] {

@@ -64,10 +64,13 @@ struct BvpLaunch {
     double* values;            // [n_obs][n_particles]
     double* aux;               // exit time
     uint8_t* failed;
+    double* basis;             // forcing-basis mode: [n_bumps][n_obs][n_particles] unit-bump integrals
 };
 
 cudaError_t launch_bvp_walkers(const BvpLaunch& L, int n_sms, cudaStream_t s);
 cudaError_t launch_bvp_walkers_strict(const BvpLaunch& L, int n_sms, cudaStream_t s);
+// Forcing-basis mode (Gaussian-bump forcing with 1..4 terms, FP64).
+cudaError_t launch_bvp_basis(const BvpLaunch& L, int n_sms, cudaStream_t s);
 
 // Stable compaction of valid walkers per segment (reduce_observation's
 // valid/valid_aux vectors, executor.cpp:93-101).  chunk_tmp: 2 * n_seg *

@@ -148,6 +148,16 @@ def main() -> None:
                                                        [0.0, 0.0, 0.0], 606, 0)).hex()}
                          for F in ([0.0, 0.0, 0.0], [1.0, -0.5, 2.0])]
 
+    # optimize_forcing (Nelder-Mead over observe_bvp, optimize.cpp:175-185) on
+    # forward_bvp_box.json's "optimize" section at 300 walkers/obs.
+    ob = specs.paper_bvp(n_particles=300)
+    ctrs = [(0.68, 0.4), (0.4, 0.68), (0.82, 0.82)]
+    for tgt in ([0.0, 0.0, 0.0], [0.2, 0.1, -0.05]):
+        r = R.optimize_forcing(ob, [0.0, 0.0, 0.0], ctrs, 4.0, tgt, 0.005, 1e-4, 250, 1.0, 606)
+        g.setdefault("optimize", []).append({"target": tgt, "argmin": hx(r["argmin"]),
+                                             "min_value": float(r["min_value"]).hex(),
+                                             "iterations": r["iterations"], "stop_reason": r["stop_reason"]})
+
     # Prior mode order (inference.cpp:24-40) and a prior draw.
     g["prior"] = {"modes8": R.prior_modes(8).tolist(), "draw8": hx(u2)}
 
