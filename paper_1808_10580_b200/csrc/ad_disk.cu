@@ -191,8 +191,8 @@ __device__ __forceinline__ void velocity_disk(const SmemCoef<T>& C, const T (&x1
     }
 }
 
-template <int K, class T, int P>
-__global__ void __launch_bounds__(kBlock, (K <= 8 ? 4 : 3)) ad_particles_disk(const AdLaunch L, const double* coef) {
+template <int K, class T, int P, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) ad_particles_disk(const AdLaunch L, const double* coef) {
     // this sample's coefficient block -> shared memory (compute type)
     __shared__ __align__(16) T staged[DiskShape<K>::n_coef];
     const int sample = blockIdx.z;
@@ -213,41 +213,50 @@ __global__ void __launch_bounds__(kBlock, (K <= 8 ? 4 : 3)) ad_particles_disk(co
                          });
 }
 
-template <int K, class T, int P>
+template <int K, class T, int P, int MINB>
 cudaError_t launch_k(const AdLaunch& L, const double* coef, cudaStream_t s) {
     const int64_t span = L.p_end - L.p_begin;
     const int64_t per_block = static_cast<int64_t>(kBlock) * P;
     const dim3 grid(static_cast<unsigned>((span + per_block - 1) / per_block), static_cast<unsigned>(L.n_obs),
                     static_cast<unsigned>(L.n_samples));
-    ad_particles_disk<K, T, P><<<grid, kBlock, 0, s>>>(L, coef);
+    ad_particles_disk<K, T, P, MINB><<<grid, kBlock, 0, s>>>(L, coef);
     return cudaGetLastError();
 }
+
+// Resident blocks per SM (register budget 65536 / (128 MINB)): two particles
+// per thread need ~250 registers.
+template <int K, int P>
+struct MinBlocks {
+    static constexpr int value = P == 2 ? 2 : (K <= 8 ? 4 : 3);
+};
 
 template <class T, int P>
 cudaError_t dispatch_p(const AdLaunch& L, int K, const double* c, cudaStream_t s) {
     switch (K) {
-        case 1: return launch_k<1, T, P>(L, c, s);
-        case 2: return launch_k<2, T, P>(L, c, s);
-        case 3: return launch_k<3, T, P>(L, c, s);
-        case 4: return launch_k<4, T, P>(L, c, s);
-        case 5: return launch_k<5, T, P>(L, c, s);
-        case 6: return launch_k<6, T, P>(L, c, s);
-        case 7: return launch_k<7, T, P>(L, c, s);
-        case 8: return launch_k<8, T, P>(L, c, s);
-        case 9: return launch_k<9, T, P>(L, c, s);
-        case 10: return launch_k<10, T, P>(L, c, s);
-        case 11: return launch_k<11, T, P>(L, c, s);
-        case 12: return launch_k<12, T, P>(L, c, s);
+        case 1: return launch_k<1, T, P, MinBlocks<1, P>::value>(L, c, s);
+        case 2: return launch_k<2, T, P, MinBlocks<2, P>::value>(L, c, s);
+        case 3: return launch_k<3, T, P, MinBlocks<3, P>::value>(L, c, s);
+        case 4: return launch_k<4, T, P, MinBlocks<4, P>::value>(L, c, s);
+        case 5: return launch_k<5, T, P, MinBlocks<5, P>::value>(L, c, s);
+        case 6: return launch_k<6, T, P, MinBlocks<6, P>::value>(L, c, s);
+        case 7: return launch_k<7, T, P, MinBlocks<7, P>::value>(L, c, s);
+        case 8: return launch_k<8, T, P, MinBlocks<8, P>::value>(L, c, s);
+        case 9: return launch_k<9, T, P, MinBlocks<9, P>::value>(L, c, s);
+        case 10: return launch_k<10, T, P, MinBlocks<10, P>::value>(L, c, s);
+        case 11: return launch_k<11, T, P, MinBlocks<11, P>::value>(L, c, s);
+        case 12: return launch_k<12, T, P, MinBlocks<12, P>::value>(L, c, s);
         default: return cudaErrorNotSupported;
     }
 }
 
 // Particles per thread: 1 by default; SMC_DISK_P=2 lets each staged
-// coefficient load feed two particles (more registers, fewer warps).
+// coefficient load feed two particles and doubles the ILP of the Box-Muller /
+// sincospi chains, but halves the threads.  Measured on C2 it lands within
+// +-2.5% of P=1 depending on the box, and loses on small launches (C1, pCN).
 template <class T>
 cudaError_t dispatch(const AdLaunch& L, int K, const double* c, cudaStream_t s) {
     const char* e = std::getenv("SMC_DISK_P");
-    const int P = (e && std::atoi(e) > 0) ? std::atoi(e) : 1;
+    const int P = (e && std::atoi(e) == 2 && K <= 11) ? 2 : 1;
     return P == 1 ? dispatch_p<T, 1>(L, K, c, s) : dispatch_p<T, 2>(L, K, c, s);
 }
 

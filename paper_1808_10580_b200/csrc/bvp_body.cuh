@@ -29,6 +29,8 @@ constexpr int kBvpBlock = 128;
 
 __device__ __forceinline__ double log_u(double x) { return fm::log_pos(x); }  // uniform in (0,1)
 __device__ __forceinline__ float log_u(float x) { return __logf(x); }
+__device__ __forceinline__ double sqrt_u(double v) { return fm::sqrt_pos(v); }
+__device__ __forceinline__ float sqrt_u(float v) { return sqrtf(v); }
 
 // Forcing f(x) evaluated every step.  NB > 0: a Gaussian-bump sum of exactly
 // NB terms held in registers for the whole walk (no per-step loads or
@@ -135,7 +137,7 @@ __global__ void __launch_bounds__(kBvpBlock) bvp_walkers(const BvpLaunch L) {
                 xi2 = r * sin(a);
                 velocity_strict<KCAP>(L.vel, p1, p2, x1, x2, v1, v2);
             } else {
-                const T rad = sqrt(T(-2) * log_u(T(u.u0)));
+                const T rad = sqrt_u(T(-2) * log_u(T(u.u0)));
                 T sn, cs;
                 sincospi_t(T(2) * T(u.u1), &sn, &cs);
                 xi1 = rad * cs;

@@ -1,0 +1,97 @@
+"""Accuracy of csrc/fastmath.cuh (the FP64 sincospi / log / exp / sqrt / divide
+the fast particle kernels use) through a host build of the same header,
+against mpmath at 40 digits.  The device build differs only in the rcp/rsqrt
+seeds (MUFU vs float), which the Newton steps wash out; the GPU tests compare
+the device Box-Muller pairs with the oracle's libm ones (test_gpu_parity.py).
+"""
+import ctypes as C
+import subprocess
+from pathlib import Path
+
+import mpmath
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+@pytest.fixture(scope="module")
+def fm(tmp_path_factory):
+    out = tmp_path_factory.mktemp("fm") / "libfm.so"
+    subprocess.run(["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-shared", "-fPIC", "-o", str(out),
+                    str(ROOT / "tests/cpp/fastmath_host.cpp")], check=True)
+    lib = C.CDLL(str(out))
+    P = C.POINTER(C.c_double)
+    for name, n in [("fm_sincospi", 4), ("fm_log", 3), ("fm_exp", 3), ("fm_sqrt", 3), ("fm_div", 4)]:
+        getattr(lib, name).restype = None
+    return lib
+
+
+def _p(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def ulp_err(got, exact):
+    got = np.asarray(got, dtype=np.float64)
+    ex = np.array([float(e) for e in exact])
+    ulp = np.spacing(np.abs(ex))
+    d = np.array([float(abs(mpmath.mpf(g) - e)) for g, e in zip(got, exact)])
+    return np.max(d / ulp)
+
+
+mpmath.mp.dps = 40
+RNG = np.random.default_rng(7)
+
+
+def test_sincospi(fm):
+    a = np.concatenate([RNG.uniform(-4, 4, 3000), RNG.uniform(0, 2, 1000), np.arange(-8, 9) * 0.25])
+    s = np.empty_like(a)
+    c = np.empty_like(a)
+    fm.fm_sincospi(_p(a), C.c_int64(a.size), _p(s), _p(c))
+    es = [mpmath.sinpi(mpmath.mpf(x)) for x in a]
+    ec = [mpmath.cospi(mpmath.mpf(x)) for x in a]
+    # absolute error in units of 2^-53 (values near zero have tiny ulps)
+    ds = max(float(abs(mpmath.mpf(g) - e)) for g, e in zip(s, es)) / 2**-53
+    dc = max(float(abs(mpmath.mpf(g) - e)) for g, e in zip(c, ec)) / 2**-53
+    assert ds <= 2.0 and dc <= 2.0
+    big = np.abs(np.array([float(e) for e in es])) > 0.25
+    assert ulp_err(s[big], [e for e, b in zip(es, big) if b]) <= 2.0
+    # exact quarter turns
+    q = np.arange(-8, 9) * 0.5
+    s = np.empty_like(q)
+    c = np.empty_like(q)
+    fm.fm_sincospi(_p(q), C.c_int64(q.size), _p(s), _p(c))
+    assert np.all(np.abs(s) == np.abs(np.round(np.sin(np.pi * q))))
+    assert np.all(np.abs(c) == np.abs(np.round(np.cos(np.pi * q))))
+
+
+def test_log_on_uniforms(fm):
+    # the kernels feed it ((r >> 11) + 0.5) 2^-53: (0, 1), down to 2^-54
+    x = np.concatenate([RNG.uniform(0, 1, 3000), 2.0 ** -RNG.uniform(1, 54, 1000),
+                        [2.0 ** -54, 0.5, 1 - 2.0 ** -53, np.sqrt(0.5), 0.7071067811865476]])
+    y = np.empty_like(x)
+    fm.fm_log(_p(x), C.c_int64(x.size), _p(y))
+    assert ulp_err(y, [mpmath.log(mpmath.mpf(v)) for v in x]) <= 2.0
+
+
+def test_exp(fm):
+    x = np.concatenate([RNG.uniform(-700, 0, 2000), RNG.uniform(-5, 5, 2000), [0.0, -1e-300]])
+    y = np.empty_like(x)
+    fm.fm_exp(_p(x), C.c_int64(x.size), _p(y))
+    assert ulp_err(y, [mpmath.exp(mpmath.mpf(v)) for v in x]) <= 2.0
+    z = np.array([-800.0, -708.5])
+    w = np.empty_like(z)
+    fm.fm_exp(_p(z), C.c_int64(2), _p(w))
+    assert w[0] == 0.0
+
+
+def test_sqrt_and_div_correctly_rounded(fm):
+    v = np.concatenate([-2 * np.log(RNG.uniform(0, 1, 4000)), [2.0 ** -53, 75.0, 1.0, 4.0]])
+    y = np.empty_like(v)
+    fm.fm_sqrt(_p(v), C.c_int64(v.size), _p(y))
+    assert np.array_equal(y, np.sqrt(v))
+    f = RNG.uniform(np.sqrt(0.5) - 1, np.sqrt(2) - 1, 4000)
+    d = 2.0 + f
+    q = np.empty_like(f)
+    fm.fm_div(_p(f), _p(d), C.c_int64(f.size), _p(q))
+    assert np.array_equal(q, f / d)
