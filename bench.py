@@ -315,7 +315,13 @@ def run_ours(args):
         my_steps = steps_per_eval * (e - b) / n_chunks  # chunk-proportional (last chunk may be partial)
 
         def device_step():
-            """One evaluation through the device-level sharded path, inputs resident."""
+            """One evaluation, inputs resident: at N=1 the single-GPU forward map
+            (K1 + K3, one launch each), at N>1 the device-level sharded path."""
+            if world == 1:
+                def run1():
+                    S.observe_ad(spec, 808, ctx=ctx)
+                    return ctx.stats().particle_kernel_ms, my_steps
+                return timed(run1)
             ops = D.DeviceOps(spec, 808, ctx)
 
             def run():

@@ -16,12 +16,12 @@ struct DomainImg {
 
 template <class T>
 __device__ __forceinline__ bool domain_contains(const DomainImg& d, T x1, T x2) {
-    if (d.kind == 1) return x1 > T(d.lo1) && x1 < T(d.hi1) && x2 > T(d.lo2) && x2 < T(d.hi2);
-    if (d.kind == 2) {
-        const T q1 = x1 - T(d.c1), q2 = x2 - T(d.c2);
-        return q1 * q1 + q2 * q2 < T(d.r2);
-    }
-    return true;
+    // both tests evaluated, then selected: no branch on the (uniform) kind in
+    // the walker loop, so the step stays one basic block
+    const bool in_box = (x1 > T(d.lo1)) & (x1 < T(d.hi1)) & (x2 > T(d.lo2)) & (x2 < T(d.hi2));
+    const T q1 = x1 - T(d.c1), q2 = x2 - T(d.c2);
+    const bool in_disk = q1 * q1 + q2 * q2 < T(d.r2);
+    return d.kind == 1 ? in_box : (d.kind == 2 ? in_disk : true);
 }
 
 template <class T>

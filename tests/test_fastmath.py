@@ -79,10 +79,15 @@ def test_exp(fm):
     y = np.empty_like(x)
     fm.fm_exp(_p(x), C.c_int64(x.size), _p(y))
     assert ulp_err(y, [mpmath.exp(mpmath.mpf(v)) for v in x]) <= 2.0
-    z = np.array([-800.0, -708.5])
+    z = np.array([-800.0, -745.5])
     w = np.empty_like(z)
     fm.fm_exp(_p(z), C.c_int64(2), _p(w))
-    assert w[0] == 0.0
+    assert w[0] == 0.0 and w[1] == 0.0
+    z = np.array([710.0, 1e14, -1e300, -708.0, 709.0])
+    w = np.empty_like(z)
+    fm.fm_exp(_p(z), C.c_int64(z.size), _p(w))
+    assert np.isinf(w[0]) and np.isinf(w[1]) and w[2] == 0.0
+    assert ulp_err(w[3:], [mpmath.exp(mpmath.mpf(v)) for v in z[3:]]) <= 2.0
 
 
 def test_sqrt_and_div_correctly_rounded(fm):
