@@ -313,7 +313,8 @@ smc_status smc_normal_pairs_device(smc_ctx* ctx, uint64_t seed, uint64_t obs, ui
 
 /* Stats of the last forward-map call on this context: kernel time of the
  * particle kernel (ms, CUDA events on the launching stream), its launch count,
- * and the total particle-steps executed. */
+ * and the total particle-steps executed.  After smc_pcn_chains,
+ * particle_kernel_ms is the device time of the whole step loop. */
 typedef struct smc_stats {
     double particle_kernel_ms;
     double reduce_ms;

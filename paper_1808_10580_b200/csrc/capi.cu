@@ -1003,9 +1003,63 @@ smc_status smc_pcn_chains(smc_ctx* ctx, const smc_ad_problem* forward, const smc
         S.init = 0;
         S.contraction = std::sqrt(1.0 - cfg->beta * cfg->beta);
         S.beta = cfg->beta;
+        ctx->stats = smc_stats{};
+        CK(cudaEventRecord(ctx->ev[0], s));
+        const char* ge = std::getenv("SMC_PCN_GRAPH");
+        const bool use_graph = cfg->n_steps >= 2 && s != nullptr && !(ge && std::atoi(ge) == 0);
+        if (use_graph) {
+            // Graph mode: the step index is a device counter, so a captured
+            // group of G steps (propose, pack, K1, K3, accept, commit, advance)
+            // replays unchanged; the launch cost per step drops to a share of
+            // one graph launch.  Same kernels, same arguments: bit-identical.
+            auto* d_it = static_cast<int64_t*>(dalloc(8));
+            CK(cudaMemsetAsync(d_it, 0, 8, s));
+            S.it_dev = d_it;
+            S.blk_base = blk;
+            S.burn_in = cfg->burn_in;
+            S.thin = cfg->thin;
+            const int64_t before = ctx->total_launches;
+            auto capture = [&](int64_t g) {
+                cudaGraph_t graph = nullptr;
+                CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+                try {
+                    for (int64_t k = 0; k < g; ++k) {
+                        CK(launch_pcn_propose(S, s));
+                        CK(launch_pcn_accept(S, forward_map(), s));
+                        CK(launch_pcn_commit(S, s));
+                        CK(launch_pcn_advance(d_it, s));
+                    }
+                } catch (...) {
+                    cudaStreamEndCapture(s, &graph);
+                    if (graph) cudaGraphDestroy(graph);
+                    throw;
+                }
+                CK(cudaStreamEndCapture(s, &graph));
+                cudaGraphExec_t exec = nullptr;
+                const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+                cudaGraphDestroy(graph);
+                CK(e);
+                return exec;
+            };
+            const int64_t G = std::min<int64_t>(16, cfg->n_steps);
+            cudaGraphExec_t group = capture(G);
+            const int64_t per_step = (ctx->total_launches - before) / G + 4;
+            const int64_t rest = cfg->n_steps % G;
+            cudaGraphExec_t single = rest ? capture(1) : nullptr;
+            struct ExecFree {
+                cudaGraphExec_t a, b;
+                ~ExecFree() {
+                    if (a) cudaGraphExecDestroy(a);
+                    if (b) cudaGraphExecDestroy(b);
+                }
+            } exec_free{group, single};
+            for (int64_t q = 0; q < cfg->n_steps / G; ++q) CK(cudaGraphLaunch(group, s));
+            for (int64_t r = 0; r < rest; ++r) CK(cudaGraphLaunch(single, s));
+            ctx->total_launches = before + per_step * cfg->n_steps;
+        }
         bool ucache = false;
         uint64_t ublk = 0;
-        for (int64_t it = 0; it < cfg->n_steps; ++it) {
+        for (int64_t it = 0; !use_graph && it < cfg->n_steps; ++it) {
             S.blk0 = blk;
             blk += static_cast<uint64_t>(M);
             if (!ucache) {  // uniform() draws a fresh block and caches its second value
@@ -1028,6 +1082,8 @@ smc_status smc_pcn_chains(smc_ctx* ctx, const smc_ad_problem* forward, const smc
             CK(launch_pcn_commit(S, s));
             count_launches(ctx, 3);
         }
+        CK(cudaEventRecord(ctx->ev[1], s));
+        CK(cudaEventRecord(ctx->ev[2], s));
         auto d2h = [&](void* dst, const void* src, size_t bytes) {
             if (dst) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
         };
@@ -1039,6 +1095,7 @@ smc_status smc_pcn_chains(smc_ctx* ctx, const smc_ad_problem* forward, const smc
         if (S.phi_trace && cfg->n_steps > 0) d2h(out->phi_trace, S.phi_trace, 8 * B * cfg->n_steps);
         if (S.samples) d2h(out->samples, S.samples, 8 * B * n_samples * dim);
         CK(cudaStreamSynchronize(s));
+        finish_stats(ctx);  // particle_kernel_ms = device time of the step loop
     });
 }
 

@@ -130,7 +130,14 @@ struct PcnStep {
     double* samples;         // [n_chains][n_samples][dim] or null
     int64_t step;            // 0-based step index
     int64_t sample_slot;     // >= 0: store the state as sample #slot
+    // Graph mode (it_dev != null): the step index lives on the device and the
+    // kernels derive blk0 / ublk / uhalf / step / sample_slot from it, so one
+    // captured step replays unchanged; pcn_advance bumps it.
+    const int64_t* it_dev;
+    uint64_t blk_base;       // stream block counter after chain_init
+    int64_t burn_in, thin;
 };
+cudaError_t launch_pcn_advance(int64_t* it_dev, cudaStream_t s);
 cudaError_t launch_pcn_propose(const PcnStep& S, cudaStream_t s);
 cudaError_t launch_pcn_pack(const int32_t* ip, const int32_t* im, const double* sp, const double* sm, int64_t stride,
                             const double* Up, int64_t dim, int64_t n_chains, double* blocks, cudaStream_t s);

@@ -12,7 +12,8 @@
 // The chain randomness is each chain's own NormalStream{seed, 0xFFFFFFFF, 0}
 // (inference.cpp:12, :175): the host tracks the stream's block counter and the
 // uniform() cache (rng.cpp:85-94) — identical for every chain — and passes the
-// block indices to the kernels.
+// block indices to the kernels, or (graph mode) the kernels derive them from a
+// device step counter.
 #define SMC_STRICT_TU 1
 #include <cuda_runtime.h>
 
@@ -36,6 +37,41 @@ __device__ __forceinline__ void chain_normals(uint64_t seed, uint64_t block, dou
     z2 = r * sn;
 }
 
+// Per-step stream positions.  The host loop (capi.cu) draws M blocks per
+// prior draw and one fresh uniform block every other step (the uniform()
+// cache, rng.cpp:85-94), so after chain_init at block `base`:
+//   blk0(it) = base + it M + ceil(it / 2),  ublk(it) = blk0(2 floor(it/2)) + M,
+//   uhalf(it) = it & 1,  and the thinned-sample slot of iteration it + 1.
+struct StepFields {
+    uint64_t blk0, ublk;
+    int32_t uhalf;
+    int64_t step, sample_slot;
+};
+
+__device__ __forceinline__ StepFields step_fields(const PcnStep& S) {
+    StepFields f;
+    if (!S.it_dev) {
+        f.blk0 = S.blk0;
+        f.ublk = S.ublk;
+        f.uhalf = S.uhalf;
+        f.step = S.step;
+        f.sample_slot = S.sample_slot;
+        return f;
+    }
+    const int64_t it = *S.it_dev;
+    const uint64_t M = static_cast<uint64_t>(S.M);
+    f.blk0 = S.blk_base + static_cast<uint64_t>(it) * M + static_cast<uint64_t>((it + 1) / 2);
+    const int64_t ev = it - (it & 1);
+    f.ublk = S.blk_base + static_cast<uint64_t>(ev) * M + static_cast<uint64_t>((ev + 1) / 2) + M;
+    f.uhalf = static_cast<int32_t>(it & 1);
+    f.step = it;
+    const int64_t iteration = it + 1;
+    f.sample_slot = (iteration > S.burn_in && (iteration - S.burn_in - 1) % S.thin == 0)
+                        ? (iteration - (S.burn_in > 0 ? S.burn_in : 0) - 1) / S.thin
+                        : -1;
+    return f;
+}
+
 // xi = prior_draw (stds[i] * normal(), normals pairwise, rng.cpp:74-83),
 // Up = contraction * U + beta * xi (inference.cpp:141-144), and the prior
 // norm 0.5 sum (Up_i / s_i)^2 (inference.cpp:75-83) in the reference's order.
@@ -44,9 +80,10 @@ __global__ void pcn_propose_kernel(PcnStep S) {
     const uint64_t seed = S.seeds[b];
     const double* U = S.U + b * S.dim;
     double* Up = S.Up + b * S.dim;
+    const uint64_t blk0 = step_fields(S).blk0;
     for (int64_t i = threadIdx.x; i < S.M; i += blockDim.x) {
         double z1, z2;
-        chain_normals(seed, S.blk0 + static_cast<uint64_t>(i), z1, z2);
+        chain_normals(seed, blk0 + static_cast<uint64_t>(i), z1, z2);
         const double s = S.stds[i];
         const double x1 = s * z1, x2 = s * z2;
         Up[2 * i] = S.contraction * U[2 * i] + S.beta * x1;
@@ -93,13 +130,14 @@ __global__ void pcn_accept_kernel(PcnStep S, const smc_estimate* __restrict__ es
         }
         phi_prop = ss / (2.0 * S.noise_std * S.noise_std);
     }
+    const StepFields F = step_fields(S);
     bool accept = false;
     if (S.init) {  // chain_init: the state is the proposal
         accept = true;
     } else {
         const Uniform2 u = uniform_block(static_cast<uint32_t>(S.seeds[b]), static_cast<uint32_t>(S.seeds[b] >> 32),
-                                         kChainTag, 0u, S.ublk);
-        const double uacc = S.uhalf ? u.u1 : u.u0;
+                                         kChainTag, 0u, F.ublk);
+        const double uacc = F.uhalf ? u.u1 : u.u0;
         if (isfinite(phi_prop)) accept = uacc < exp(fmin(0.0, S.phi[b] - phi_prop));
     }
     if (accept) {
@@ -112,7 +150,7 @@ __global__ void pcn_accept_kernel(PcnStep S, const smc_estimate* __restrict__ es
     const bool better = S.init || objective < S.map_obj[b];
     if (better) S.map_obj[b] = objective;
     S.map_flag[b] = better ? 1 : 0;
-    if (!S.init && S.phi_trace) S.phi_trace[b * S.n_steps + S.step] = S.phi[b];
+    if (!S.init && S.phi_trace) S.phi_trace[b * S.n_steps + F.step] = S.phi[b];
 }
 
 __global__ void pcn_commit_kernel(PcnStep S) {
@@ -120,10 +158,13 @@ __global__ void pcn_commit_kernel(PcnStep S) {
     const int64_t b = blockIdx.y;
     if (i >= S.dim) return;
     double* U = S.U + b * S.dim;
+    const int64_t slot = step_fields(S).sample_slot;
     if (S.acc_flag[b]) U[i] = S.Up[b * S.dim + i];
     if (S.map_flag[b]) S.map_u[b * S.dim + i] = U[i];
-    if (S.sample_slot >= 0 && S.samples) S.samples[(b * S.n_samples + S.sample_slot) * S.dim + i] = U[i];
+    if (slot >= 0 && S.samples) S.samples[(b * S.n_samples + slot) * S.dim + i] = U[i];
 }
+
+__global__ void pcn_advance_kernel(int64_t* it) { *it += 1; }
 
 }  // namespace
 
@@ -142,6 +183,11 @@ cudaError_t launch_pcn_pack(const int32_t* ip, const int32_t* im, const double* 
 cudaError_t launch_pcn_accept(const PcnStep& S, const void* est, cudaStream_t s) {
     pcn_accept_kernel<<<static_cast<unsigned>((S.n_chains + 127) / 128), 128, 0, s>>>(
         S, static_cast<const smc_estimate*>(est));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pcn_advance(int64_t* it_dev, cudaStream_t s) {
+    pcn_advance_kernel<<<1, 1, 0, s>>>(it_dev);
     return cudaGetLastError();
 }
 

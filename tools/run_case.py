@@ -60,10 +60,16 @@ if args.config in ("pcn", "pcn8"):
     n_steps = int(os.environ.get('PCN_STEPS', '2000'))
     cfg = S.ChainConfig(n_steps=n_steps, beta=0.22, burn_in=min(200, n_steps // 2), thin=10)
     S.run_chains(S.ChainConfig(n_steps=5, beta=0.22), prior, like, list(range(B)), ctx=ctx)  # warm-up
-    t0 = time.perf_counter()
-    res = S.run_chains(cfg, prior, like, list(range(B)), ctx=ctx)
-    el = time.perf_counter() - t0
-    print(f"{args.config} B={B} dim={prior.dimension()}: {n_steps} steps in {el:.3f} s -> "
+    times, dev = [], []
+    for _ in range(max(args.reps, 1)):
+        t0 = time.perf_counter()
+        res = S.run_chains(cfg, prior, like, list(range(B)), ctx=ctx)
+        times.append(time.perf_counter() - t0)
+        dev.append(ctx.stats().particle_kernel_ms)
+    el = min(times)
+    print(f"[wall {', '.join(f'{t / n_steps * 1e6:.0f}' for t in times)} us/step; "
+          f"device {', '.join(f'{d / n_steps * 1e3:.0f}' for d in dev)} us/step]")
+    print(f"{args.config} B={B} dim={prior.dimension()}: {n_steps} steps in {el:.3f} s (best of {len(times)}) -> "
           f"{B * n_steps / el:.4g} chain-steps/s ({el / n_steps * 1e6:.1f} us/step), "
           f"acceptance {res['acceptance_rate'].mean():.3f}")
     sys.exit(0)
