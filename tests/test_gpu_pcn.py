@@ -60,3 +60,18 @@ def test_chain_validation(ctx):
         S.run_chains(S.ChainConfig(n_steps=3, beta=1.5), prior, likelihood(), [1], ctx=ctx)
     with pytest.raises(ValueError, match="thin must be"):
         S.run_chains(S.ChainConfig(n_steps=3, beta=0.1, thin=0), prior, likelihood(), [1], ctx=ctx)
+
+
+@pytest.mark.parametrize("n_steps,burn_in,thin", [(37, 5, 3), (16, 0, 1), (33, -2, 4)])
+def test_graph_replay_matches_step_loop(ctx, monkeypatch, n_steps, burn_in, thin):
+    """The CUDA-graph path (device step counter, 16-step groups + remainder)
+    must be bit-identical to the per-step host loop."""
+    prior = S.PriorSpec(2, 0.6, 2.5)
+    cfg = S.ChainConfig(n_steps=n_steps, beta=0.3, burn_in=burn_in, thin=thin)
+    seeds = [3, 4, 5]
+    monkeypatch.setenv("SMC_PCN_GRAPH", "0")
+    loop = S.run_chains(cfg, prior, likelihood(), seeds, ctx=ctx)
+    monkeypatch.setenv("SMC_PCN_GRAPH", "1")
+    graph = S.run_chains(cfg, prior, likelihood(), seeds, ctx=ctx)
+    for key in ("phi_trace", "final_u", "map_u", "map_objective", "accepted", "samples"):
+        assert np.array_equal(np.asarray(loop[key]), np.asarray(graph[key])), key
