@@ -129,6 +129,7 @@ struct smc_ctx {
     int64_t total_launches = 0;
     cudaEvent_t ev[4] = {};
     DevBuf image, values, aux, flags, flags2, scratch, sums, means, sumsq, sumaux, est, counts, tmp_a, tmp_b, tmp_c;
+    DevBuf pk_ip, pk_im, pk_kp, pk_km, pk_ms, pk_u, pk_blocks, pk_bad;  // device u -> field packing
     PinnedBuf staging, est_host;
     smc_stats stats{};
     // sharded AD state (smc_ad_shard_*)
@@ -449,6 +450,26 @@ void run_bvp(smc_ctx* ctx, BvpLaunch& L, int64_t n_obs, int64_t n) {
 
 }  // namespace
 
+namespace smc {
+namespace {
+// Upload a PackMap into the context's pack buffers (reused across calls).
+PackDev upload_pack_map(smc_ctx* ctx, const PackMap& m) {
+    const size_t n = static_cast<size_t>(m.stride);
+    auto* ip = ctx->pk_ip.get<int32_t>(n);
+    auto* im = ctx->pk_im.get<int32_t>(n);
+    auto* kp = ctx->pk_kp.get<double>(n);
+    auto* km = ctx->pk_km.get<double>(n);
+    auto* ms = ctx->pk_ms.get<int8_t>(n);
+    CK(cudaMemcpyAsync(ip, m.ip.data(), 4 * n, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(im, m.im.data(), 4 * n, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(kp, m.kp.data(), 8 * n, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(km, m.km.data(), 8 * n, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ms, m.ms.data(), n, cudaMemcpyHostToDevice, ctx->stream));
+    return PackDev{m.stride, ip, im, kp, km, ms};
+}
+}  // namespace
+}  // namespace smc
+
 extern "C" {
 
 int smc_abi_version(void) { return SMC_ABI_VERSION; }
@@ -572,28 +593,6 @@ smc_status smc_ad_observe_batched(smc_ctx* ctx, const smc_ad_problem* base, cons
         CK(cudaSetDevice(ctx->device));
         if (n_samples < 1) raise(SMC_EINVAL, "observe_ad_batched: need at least one sample");
         if (prior->cutoff <= 0) raise(SMC_EINVAL, "FourierVelocityField: max_wavenumber must be positive");
-        const std::vector<HostMode> pm = prior_modes(prior->cutoff);
-        const int64_t dim = 2 * static_cast<int64_t>(pm.size());
-        // One FourierVelocityField per sample, from u in prior order
-        // (velocity_from_coefficients, inference.cpp:63-73).
-        std::vector<PreparedVelocity> fields(static_cast<size_t>(n_samples));
-        std::vector<const PreparedVelocity*> fills;
-        fills.reserve(static_cast<size_t>(n_samples));
-        for (int64_t b = 0; b < n_samples; ++b) {
-            smc_velocity sv{};
-            std::vector<int32_t> k(static_cast<size_t>(dim));
-            for (size_t i = 0; i < pm.size(); ++i) {
-                k[2 * i] = pm[i].k1;
-                k[2 * i + 1] = pm[i].k2;
-            }
-            sv.is_constant = 0;
-            sv.max_wavenumber = prior->cutoff;
-            sv.n_modes = static_cast<int64_t>(pm.size());
-            sv.k = k.data();
-            sv.coeff = u + b * dim;
-            fields[static_cast<size_t>(b)] = prepare_velocity(sv);
-            fills.push_back(&fields[static_cast<size_t>(b)]);
-        }
         smc_ad_problem p = *base;
         p.velocity.is_constant = 0;
         p.velocity.max_wavenumber = prior->cutoff;
@@ -605,7 +604,36 @@ smc_status smc_ad_observe_batched(smc_ctx* ctx, const smc_ad_problem* base, cons
         if (p.precision == SMC_FP64_STRICT) raise(SMC_EINVAL, "strict precision is single-sample only");
         ctx->stats = smc_stats{};
         const int64_t n = p.n_particles, n_obs = p.n_obs;
-        AdPrepared P = prepare_ad(ctx, p, fills, fields[0], 0, n_obs);
+        // One FourierVelocityField per sample from u in prior order
+        // (velocity_from_coefficients, inference.cpp:63-73), built on the
+        // device: the image carries the full prior disk's structure and the
+        // pack kernel writes every sample's coefficient block from u.
+        const PreparedVelocity structure = prior_structure(prior->cutoff);
+        const int64_t dim = 2 * static_cast<int64_t>(structure.modes.size());
+        AdPrepared P = prepare_ad(ctx, p, {&structure}, structure, 0, n_obs);
+        const LatticeHost Lh = lattice_structure(structure);
+        const PackMap pmap = pack_map(prior->cutoff, P.disk_K > 0, &Lh);
+        const PackDev pdev = upload_pack_map(ctx, pmap);
+        double* d_u = ctx->pk_u.get<double>(static_cast<size_t>(n_samples * dim));
+        CK(cudaMemcpyAsync(d_u, u, sizeof(double) * n_samples * dim, cudaMemcpyHostToDevice, ctx->stream));
+        double* blocks = ctx->pk_blocks.get<double>(static_cast<size_t>(n_samples * pmap.stride));
+        int* d_bad = ctx->pk_bad.get<int>(1);
+        CK(cudaMemsetAsync(d_bad, 0, sizeof(int), ctx->stream));
+        for (int64_t b0 = 0; b0 < n_samples; b0 += 65535)
+            CK(launch_pack(pdev, d_u + b0 * dim, dim, std::min<int64_t>(65535, n_samples - b0),
+                           blocks + b0 * pmap.stride, d_bad, ctx->stream));
+        count_launches(ctx, (n_samples + 65534) / 65535);
+        // the FourierVelocityField ctor throws before any particle work (fields.cpp:46-47)
+        int bad = 0;
+        CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (bad) raise(SMC_EINVAL, "FourierVelocityField: non-finite coefficient");
+        if (P.disk_K > 0) {
+            P.disk = blocks;
+        } else {
+            P.L.vel.lat.coef = blocks;
+            P.L.vel.lat.sample_stride = pmap.stride;
+        }
         uint64_t* d_seeds = nullptr;
         if (seeds) {
             d_seeds = ctx->tmp_a.get<uint64_t>(static_cast<size_t>(n_samples));
@@ -816,75 +844,12 @@ smc_status smc_pcn_chains(smc_ctx* ctx, const smc_ad_problem* forward, const smc
             stds[static_cast<size_t>(i)] = prior->s0 * std::pow(kn, -prior->alpha);
         }
         // lattice structure of the full prior disk and the u -> block gather map
-        PreparedVelocity structure;
-        structure.is_constant = false;
-        structure.K = prior->cutoff;
-        for (const auto& m : pm) structure.modes.push_back(HostMode{m.k1, m.k2, 1.0, 0.0});
-        std::sort(structure.modes.begin(), structure.modes.end(), [](const HostMode& a, const HostMode& b) {
-            return a.k1 != b.k1 ? a.k1 < b.k1 : a.k2 < b.k2;
-        });
-        // u -> coefficient-block gather map, in the disk layout (disk_shape.h,
-        // K <= kDiskMaxK) or the tiled lattice layout (images.h)
+        // (disk layout for K <= kDiskMaxK, tiled lattice otherwise)
+        const PreparedVelocity structure = prior_structure(prior->cutoff);
         const bool use_disk = prior->cutoff <= kDiskMaxK && std::getenv("SMC_DISABLE_DISK") == nullptr;
         const LatticeHost Lh = lattice_structure(structure);
-        const int64_t stride = use_disk ? disk_n_coef(prior->cutoff) : Lh.stride;
-        std::vector<int32_t> ip(static_cast<size_t>(stride), -1), imv(static_cast<size_t>(stride), -1);
-        std::vector<double> sp(static_cast<size_t>(stride), 0.0), sm(static_cast<size_t>(stride), 0.0);
-        {
-            const int K = prior->cutoff;
-            std::vector<int32_t> idx(static_cast<size_t>((K + 1) * (2 * K + 1)), -1);
-            auto at = [&](int k1, int k2) -> int32_t& { return idx[static_cast<size_t>(k1 * (2 * K + 1) + k2 + K)]; };
-            for (int64_t i = 0; i < M; ++i) at(pm[i].k1, pm[i].k2) = static_cast<int32_t>(i);
-            auto g = [&](int k1, int k2) { return 2.0 / std::sqrt(double(k1) * k1 + double(k2) * k2); };
-            auto set = [&](int64_t slot, int k1p, int k2p, int k1m, int k2m, int part, double msign) {
-                if (k2p <= K && k2p >= -K && at(k1p, k2p) >= 0) {
-                    ip[slot] = 2 * at(k1p, k2p) + part;
-                    sp[slot] = g(k1p, k2p);
-                }
-                if (k1m >= 0 && k2m <= K && k2m >= -K && at(k1m, k2m) >= 0) {
-                    imv[slot] = 2 * at(k1m, k2m) + part;
-                    sm[slot] = msign * g(k1m, k2m);
-                }
-            };
-            auto pair = [&](int64_t base, int k1, int j) {
-                set(base + 0, k1, j, k1, -j, 0, 1.0);   // alpha_re
-                set(base + 1, k1, j, k1, -j, 1, 1.0);   // alpha_im
-                set(base + 2, k1, j, k1, -j, 0, -1.0);  // beta_re
-                set(base + 3, k1, j, k1, -j, 1, -1.0);  // beta_im
-            };
-            if (use_disk) {
-                int64_t pidx = 0;
-                for (int k1 = 1; k1 <= K; ++k1)
-                    for (int j = 1; j <= disk_jmax(K, k1); ++j, ++pidx) pair(4 * pidx, k1, j);
-                const int64_t row0 = 4 * disk_n_pairs(K), g0 = row0 + 2 * K;
-                for (int j = 1; j <= K; ++j) {
-                    set(row0 + 2 * (j - 1), 0, j, -1, 0, 0, 0.0);
-                    set(row0 + 2 * (j - 1) + 1, 0, j, -1, 0, 1, 0.0);
-                }
-                for (int k1 = 1; k1 <= K; ++k1) {
-                    set(g0 + 2 * (k1 - 1), k1, 0, -1, 0, 0, 0.0);
-                    set(g0 + 2 * (k1 - 1) + 1, k1, 0, -1, 0, 1, 0.0);
-                }
-            } else {
-                for (int t = 0; t < Lh.n_tiles; ++t) {
-                    const int2 tl = Lh.tiles[static_cast<size_t>(t)];
-                    for (int k1 = 1; k1 <= tl.x; ++k1)
-                        for (int q = 0; q < kLatticeTileHost; ++q) {
-                            const int j = kLatticeTileHost * t + q + 1;
-                            if (j > K) break;
-                            pair(tl.y + static_cast<int64_t>(k1 - 1) * kLatticeTileHost * 4 + 4 * q, k1, j);
-                        }
-                }
-                for (int j = 1; j <= Lh.J0; ++j) {
-                    set(Lh.row0_off + 2 * (j - 1), 0, j, -1, 0, 0, 0.0);
-                    set(Lh.row0_off + 2 * (j - 1) + 1, 0, j, -1, 0, 1, 0.0);
-                }
-                for (int k1 = 1; k1 <= Lh.R; ++k1) {
-                    set(Lh.g0_off + 2 * k1, k1, 0, -1, 0, 0, 0.0);
-                    set(Lh.g0_off + 2 * k1 + 1, k1, 0, -1, 0, 1, 0.0);
-                }
-            }
-        }
+        const PackMap pmap = pack_map(prior->cutoff, use_disk, &Lh);
+        const int64_t stride = pmap.stride;
         if (static_cast<int64_t>(p.n_obs) <= 0) raise(SMC_EINVAL, "AdProblemSpec: no observations");
 
         // device buffers (freed at the end of the call)
@@ -923,14 +888,7 @@ smc_status smc_pcn_chains(smc_ctx* ctx, const smc_ad_problem* forward, const smc
         auto* d_data = static_cast<double*>(dalloc(8 * n_obs));
         h2d(d_data, data, 8 * n_obs);
         S.data = d_data;
-        auto* d_ip = static_cast<int32_t*>(dalloc(4 * stride));
-        auto* d_im = static_cast<int32_t*>(dalloc(4 * stride));
-        auto* d_sp = static_cast<double*>(dalloc(8 * stride));
-        auto* d_sm = static_cast<double*>(dalloc(8 * stride));
-        h2d(d_ip, ip.data(), 4 * stride);
-        h2d(d_im, imv.data(), 4 * stride);
-        h2d(d_sp, sp.data(), 8 * stride);
-        h2d(d_sm, sm.data(), 8 * stride);
+        const PackDev pdev = upload_pack_map(ctx, pmap);
         S.U = static_cast<double*>(dalloc(8 * B * dim));
         S.Up = static_cast<double*>(dalloc(8 * B * dim));
         S.map_u = static_cast<double*>(dalloc(8 * B * dim));
@@ -962,7 +920,9 @@ smc_status smc_pcn_chains(smc_ctx* ctx, const smc_ad_problem* forward, const smc
         double* values = ctx->values.get<double>(static_cast<size_t>(B * n_obs * n));
 
         auto forward_map = [&]() -> smc_estimate* {
-            CK(launch_pcn_pack(d_ip, d_im, d_sp, d_sm, stride, S.Up, dim, B, d_blocks, s));
+            for (int64_t b0 = 0; b0 < B; b0 += 65535)
+                CK(launch_pack(pdev, S.Up + b0 * dim, dim, std::min<int64_t>(65535, B - b0), d_blocks + b0 * stride,
+                               nullptr, s));
             constexpr int64_t kMaxZ = 65535;
             for (int64_t b0 = 0; b0 < B; b0 += kMaxZ) {
                 AdLaunch L = P.L;

@@ -281,6 +281,86 @@ std::vector<HostMode> prior_modes(int cutoff) {
     return out;
 }
 
+PreparedVelocity prior_structure(int cutoff) {
+    PreparedVelocity v;
+    v.is_constant = false;
+    v.K = cutoff;
+    for (const auto& m : prior_modes(cutoff)) v.modes.push_back(HostMode{m.k1, m.k2, 1.0, 0.0});
+    std::sort(v.modes.begin(), v.modes.end(), [](const HostMode& a, const HostMode& b) {
+        return a.k1 != b.k1 ? a.k1 < b.k1 : a.k2 < b.k2;
+    });
+    return v;
+}
+
+PackMap pack_map(int K, bool disk, const LatticeHost* lattice) {
+    const std::vector<HostMode> pm = prior_modes(K);
+    std::vector<int32_t> idx(static_cast<size_t>((K + 1) * (2 * K + 1)), -1);
+    auto at = [&](int k1, int k2) -> int32_t& { return idx[static_cast<size_t>(k1 * (2 * K + 1) + k2 + K)]; };
+    for (size_t i = 0; i < pm.size(); ++i) at(pm[i].k1, pm[i].k2) = static_cast<int32_t>(i);
+    auto kn = [](int k1, int k2) { return std::sqrt(double(k1) * k1 + double(k2) * k2); };
+    PackMap m;
+    m.stride = disk ? disk_n_coef(K) : lattice->stride;
+    const size_t n = static_cast<size_t>(m.stride);
+    m.ip.assign(n, -1);
+    m.im.assign(n, -1);
+    m.kp.assign(n, 1.0);
+    m.km.assign(n, 1.0);
+    m.ms.assign(n, 0);
+    auto present = [&](int k1, int k2) { return k1 >= 0 && k2 >= -K && k2 <= K && at(k1, k2) >= 0; };
+    // single mode (k1, k2), real or imaginary part
+    auto single = [&](int64_t slot, int k1, int k2, int part) {
+        if (!present(k1, k2)) return;
+        m.ip[slot] = 2 * at(k1, k2) + part;
+        m.kp[slot] = kn(k1, k2);
+    };
+    // the 4 slots of a +/-j pair: alpha_re, alpha_im, beta_re, beta_im
+    auto pair = [&](int64_t base, int k1, int j) {
+        for (int q = 0; q < 4; ++q) {
+            const int part = q & 1;
+            single(base + q, k1, j, part);
+            m.ms[base + q] = q < 2 ? 1 : -1;
+            if (present(k1, -j)) {
+                m.im[base + q] = 2 * at(k1, -j) + part;
+                m.km[base + q] = kn(k1, -j);
+            }
+        }
+    };
+    if (disk) {  // disk_fill's slot order
+        int64_t p = 0;
+        for (int k1 = 1; k1 <= K; ++k1)
+            for (int j = 1; j <= disk_jmax(K, k1); ++j, ++p) pair(4 * p, k1, j);
+        const int64_t row0 = 4 * disk_n_pairs(K), g0 = row0 + 2 * K;
+        for (int j = 1; j <= K; ++j) {
+            single(row0 + 2 * (j - 1), 0, j, 0);
+            single(row0 + 2 * (j - 1) + 1, 0, j, 1);
+        }
+        for (int k1 = 1; k1 <= K; ++k1) {
+            single(g0 + 2 * (k1 - 1), k1, 0, 0);
+            single(g0 + 2 * (k1 - 1) + 1, k1, 0, 1);
+        }
+    } else {  // lattice_fill's slot order
+        const LatticeHost& s = *lattice;
+        for (int t = 0; t < s.n_tiles; ++t) {
+            const int2 tl = s.tiles[static_cast<size_t>(t)];
+            for (int k1 = 1; k1 <= tl.x; ++k1)
+                for (int q = 0; q < kTileW; ++q) {
+                    const int j = kTileW * t + q + 1;
+                    if (j > K) break;
+                    pair(tl.y + static_cast<int64_t>(k1 - 1) * kTileW * 4 + 4 * q, k1, j);
+                }
+        }
+        for (int j = 1; j <= s.J0; ++j) {
+            single(s.row0_off + 2 * (j - 1), 0, j, 0);
+            single(s.row0_off + 2 * (j - 1) + 1, 0, j, 1);
+        }
+        for (int k1 = 1; k1 <= s.R; ++k1) {
+            single(s.g0_off + 2 * k1, k1, 0, 0);
+            single(s.g0_off + 2 * k1 + 1, k1, 0, 1);
+        }
+    }
+    return m;
+}
+
 AdObsImg make_ad_obs(double t, double x1, double x2, double dt, double sigma) {
     AdObsImg o;
     o.x1 = x1;

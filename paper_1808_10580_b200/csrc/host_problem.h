@@ -58,6 +58,23 @@ void disk_fill(int K, const PreparedVelocity& v, double* dst);
 // PriorSpec::modes (src/inference.cpp:24-40).
 std::vector<HostMode> prior_modes(int cutoff);
 
+// Gather map u (prior order, velocity_from_coefficients, inference.cpp:63-73)
+// -> coefficient block (disk or tiled-lattice layout), so the blocks of many
+// parameter samples are packed on the device.  Slot q of a block is
+//   v = (ip[q] >= 0 ? 2 u[ip[q]] / kp[q] : 0);
+//   if (ms[q] != 0) v = v +/- (im[q] >= 0 ? 2 u[im[q]] / km[q] : 0)
+// evaluated without contraction: the same operations lattice_fill/disk_fill
+// perform on the field built from u, so the blocks are bit-identical.
+struct PackMap {
+    int64_t stride = 0;
+    std::vector<int32_t> ip, im;
+    std::vector<double> kp, km;
+    std::vector<int8_t> ms;  // +1: alpha (g+ + g-), -1: beta (g+ - g-), 0: single mode
+};
+PackMap pack_map(int cutoff, bool disk, const LatticeHost* lattice);
+// Full prior disk as a mode list (coefficients 1), for the layout structure.
+PreparedVelocity prior_structure(int cutoff);
+
 // Step schedule of one AD observation (sde.cpp:42-45).
 AdObsImg make_ad_obs(double t, double x1, double x2, double dt, double sigma);
 

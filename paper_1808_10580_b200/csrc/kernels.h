@@ -139,8 +139,18 @@ struct PcnStep {
 };
 cudaError_t launch_pcn_advance(int64_t* it_dev, cudaStream_t s);
 cudaError_t launch_pcn_propose(const PcnStep& S, cudaStream_t s);
-cudaError_t launch_pcn_pack(const int32_t* ip, const int32_t* im, const double* sp, const double* sm, int64_t stride,
-                            const double* Up, int64_t dim, int64_t n_chains, double* blocks, cudaStream_t s);
+// u -> coefficient blocks on the device (host_problem.h PackMap, uploaded).
+// grid.y = n_samples <= 65535 per launch.
+struct PackDev {
+    int64_t stride;
+    const int32_t* ip;
+    const int32_t* im;
+    const double* kp;
+    const double* km;
+    const int8_t* ms;
+};
+cudaError_t launch_pack(const PackDev& M, const double* Up, int64_t dim, int64_t n_samples, double* blocks, int* bad,
+                        cudaStream_t s);
 cudaError_t launch_pcn_accept(const PcnStep& S, const void* est, cudaStream_t s);
 cudaError_t launch_pcn_commit(const PcnStep& S, cudaStream_t s);
 

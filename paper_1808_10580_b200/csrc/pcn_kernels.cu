@@ -100,20 +100,35 @@ __global__ void pcn_propose_kernel(PcnStep S) {
     }
 }
 
-// velocity_from_coefficients -> tiled lattice block (images.h layout):
-// slot q of sample b = sp * u[ip] + sm * u[im] (indices -1 contribute 0).
-__global__ void pcn_pack_kernel(const int32_t* __restrict__ ip, const int32_t* __restrict__ im,
-                                const double* __restrict__ sp, const double* __restrict__ sm, int64_t stride,
-                                const double* __restrict__ Up, int64_t dim, double* __restrict__ blocks) {
+// velocity_from_coefficients -> coefficient blocks through the host-built
+// gather map (host_problem.h PackMap): the operations of lattice_fill /
+// disk_fill, uncontracted (this TU is -fmad=false), so the blocks equal the
+// host-filled ones bit for bit.  A non-finite coefficient raises *bad (the
+// FourierVelocityField ctor check, fields.cpp:46-47).
+__global__ void pcn_pack_kernel(PackDev M, const double* __restrict__ Up, int64_t dim, double* __restrict__ blocks,
+                                int* bad) {
     const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t b = blockIdx.y;
-    if (q >= stride) return;
+    if (q >= M.stride) return;
     const double* u = Up + b * dim;
+    const int32_t a = M.ip[q], c = M.im[q];
+    const int ms = M.ms[q];
     double v = 0.0;
-    const int32_t a = ip[q], c = im[q];
-    if (a >= 0) v = sp[q] * u[a];
-    if (c >= 0) v = v + sm[q] * u[c];
-    blocks[b * stride + q] = v;
+    if (a >= 0) {
+        const double x = u[a];
+        if (bad && !isfinite(x)) *bad = 1;
+        v = 2.0 * x / M.kp[q];
+    }
+    if (ms != 0) {
+        double g = 0.0;
+        if (c >= 0) {
+            const double x = u[c];
+            if (bad && !isfinite(x)) *bad = 1;
+            g = 2.0 * x / M.km[q];
+        }
+        v = ms > 0 ? v + g : v - g;
+    }
+    blocks[b * M.stride + q] = v;
 }
 
 // misfit (inference.cpp:98-103), the chain's uniform, the accept rule
@@ -173,10 +188,10 @@ cudaError_t launch_pcn_propose(const PcnStep& S, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_pcn_pack(const int32_t* ip, const int32_t* im, const double* sp, const double* sm, int64_t stride,
-                            const double* Up, int64_t dim, int64_t n_chains, double* blocks, cudaStream_t s) {
-    const dim3 grid(static_cast<unsigned>((stride + 255) / 256), static_cast<unsigned>(n_chains));
-    pcn_pack_kernel<<<grid, 256, 0, s>>>(ip, im, sp, sm, stride, Up, dim, blocks);
+cudaError_t launch_pack(const PackDev& M, const double* Up, int64_t dim, int64_t n_samples, double* blocks, int* bad,
+                        cudaStream_t s) {
+    const dim3 grid(static_cast<unsigned>((M.stride + 255) / 256), static_cast<unsigned>(n_samples));
+    pcn_pack_kernel<<<grid, 256, 0, s>>>(M, Up, dim, blocks, bad);
     return cudaGetLastError();
 }
 

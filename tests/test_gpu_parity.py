@@ -374,3 +374,16 @@ def test_bvp_fp32_within_three_standard_errors(ctx, golden):
     for e, r in zip(S.observe_bvp(spec, 606, ctx=ctx), golden["bvp_box"]["estimates"]):
         r = est_from(r)
         assert abs(e.mean - r["mean"]) <= 3.0 * r["std_error"]
+
+
+def test_batched_non_finite_coefficient_rejected(ctx):
+    """velocity_from_coefficients -> FourierVelocityField ctor (fields.cpp:46-47)
+    throws std::invalid_argument before any work; the device packer checks
+    every coefficient it reads."""
+    prior = S.PriorSpec(3, 1.0, 2.0)
+    U = np.zeros((4, prior.dimension()))
+    U[2, 5] = np.inf
+    with pytest.raises(ValueError, match="non-finite coefficient"):
+        S.observe_ad_batched(specs.c4_base(n_particles=64), prior, U, 1, ctx=ctx)
+    U[2, 5] = 0.0
+    S.observe_ad_batched(specs.c4_base(n_particles=64), prior, U, 1, ctx=ctx)  # context still usable
