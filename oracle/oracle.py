@@ -283,6 +283,53 @@ class Reference(_Checker):
         return out.value
 
 
+class ReferenceCli:
+    """The reference's config parser, record writer and CLI command bodies
+    (oracle/ref_cli.cpp over the compiled reference; needs config.cpp, i.e.
+    nlohmann::json at build time)."""
+
+    KINDS = {0: None, 1: "ConfigError", 2: "invalid_argument", 3: "out_of_range", 4: "exception"}
+
+    def __init__(self, path: Path = REF_LIB):
+        self.lib = C.CDLL(str(path))
+        if not hasattr(self.lib, "refcli_config_check"):
+            raise RuntimeError("reference built without config.cpp (nlohmann::json not found)")
+
+    def config_check(self, text: str, origin: str = "<config>", stage: int = 0):
+        """-> (kind, message): kind None (accepted), "ConfigError",
+        "invalid_argument", "out_of_range" or "exception"."""
+        buf = C.create_string_buffer(4096)
+        rc = self.lib.refcli_config_check(text.encode(), origin.encode(), stage, buf, 4096)
+        return self.KINDS[rc], buf.value.decode()
+
+    def format_double(self, v: float) -> str:
+        buf = C.create_string_buffer(64)
+        self.lib.refcli_format_double(C.c_double(v), buf, 64)
+        return buf.value.decode()
+
+    def _run(self, fn, *args):
+        msg = C.create_string_buffer(4096)
+        rc = fn(*args, msg, 4096)
+        if rc:
+            raise RuntimeError(f"{self.KINDS[rc]}: {msg.value.decode()}")
+
+    def forward(self, config: str, out: str, fmt: str = "csv", seed: int = -1, bvp: bool = False) -> None:
+        self._run(self.lib.refcli_forward, config.encode(), out.encode(), fmt.encode(), C.c_int64(seed), int(bvp))
+
+    def sample(self, config: str, out_dir: str, fmt: str = "csv", seed: int = -1, steps: int = -1,
+               beta: float = -1.0) -> str:
+        text = C.create_string_buffer(4096)
+        self._run(self.lib.refcli_sample, config.encode(), out_dir.encode(), fmt.encode(), C.c_int64(seed),
+                  C.c_int64(steps), C.c_double(beta), text, 4096)
+        return text.value.decode()
+
+    def optimize(self, config: str, out: str, fmt: str = "csv", seed: int = -1) -> str:
+        text = C.create_string_buffer(4096)
+        self._run(self.lib.refcli_optimize, config.encode(), out.encode(), fmt.encode(), C.c_int64(seed), text,
+                  4096)
+        return text.value.decode()
+
+
 def port_available() -> bool:
     return PORT_LIB.exists()
 
