@@ -243,6 +243,42 @@ smc_status smc_pcn_chains(smc_ctx* ctx, const smc_ad_problem* forward, const smc
                           double noise_std, uint64_t forward_seed, int64_t n_chains, const uint64_t* chain_seeds,
                           const double* u0, const smc_chain_config* cfg, smc_chain_outputs* out);
 
+/* ---- spectral Galerkin reference solver ---------
+ * galerkin_solve_ad (include/scalarmc/galerkin.hpp:36-40,
+ * src/galerkin.cpp:159-227): project theta_0 onto the Fourier basis, assemble
+ * the dense system A_lm = -vhat_{l-m}.(2 pi i m) - delta_lm kappa (2 pi |l|)^2,
+ * integrate Theta_i = (I + dt A) Theta_{i-1} through the sorted observation
+ * times (shortened steps land exactly on each t_j) and evaluate
+ * Re sum_l Theta_l(t_j) e^{2 pi i l.x_j}.  A lives in HBM/L2; each explicit
+ * Euler step is one fused complex GEMV + axpy kernel, replayed from a CUDA
+ * graph.  Basis modes: k1 = -L..L outer, k2 = -L..L inner, disk keeps
+ * |k|_2 <= L (galerkin.cpp:20-33). */
+typedef struct smc_galerkin_basis { /* GalerkinBasis (galerkin.hpp:14-18) */
+    int32_t kind;   /* 0 box, 1 disk */
+    int32_t cutoff;
+} smc_galerkin_basis;
+
+typedef struct smc_galerkin_result { /* GalerkinResult (galerkin.hpp:20-27); caller-owned arrays */
+    double* observation_values;            /* [n_obs] (required) */
+    double* coefficients_at_observations;  /* [n_obs][n_basis][2] or NULL */
+    double* final_coefficients;            /* [n_basis][2] or NULL */
+    double dt_used;
+    int64_t steps;
+} smc_galerkin_result;
+
+/* Number of basis modes and the mode list [n][2] (host only). */
+int64_t smc_galerkin_n_basis(const smc_galerkin_basis* basis);
+smc_status smc_galerkin_modes(const smc_galerkin_basis* basis, int32_t* modes);
+/* galerkin_spectral_radius (galerkin.cpp:151-157): Gershgorin row-sum bound. */
+smc_status smc_galerkin_spectral_radius(smc_ctx* ctx, const smc_ad_problem* prob, const smc_galerkin_basis* basis,
+                                        double* out);
+smc_status smc_galerkin_solve_ad(smc_ctx* ctx, const smc_ad_problem* prob, const smc_galerkin_basis* basis,
+                                 double dt_ref, smc_galerkin_result* out);
+/* galerkin_field_grid (galerkin.cpp:233-250): Re sum_l c_l e^{2 pi i l.(i/n, j/n)}
+ * on an n x n grid (row-major, x2 fastest) from coefficients in basis order. */
+smc_status smc_galerkin_field_grid(smc_ctx* ctx, const smc_galerkin_basis* basis, const double* coefficients,
+                                   int32_t n, double* grid);
+
 /* ---- resolved step sizes (host only, no device needed) ------------------- */
 /* AdProblemSpec::resolved_dt (forward_ad.cpp:10-15). */
 smc_status smc_ad_resolved_dt(const smc_ad_problem* prob, double* out);

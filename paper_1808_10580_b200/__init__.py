@@ -33,6 +33,11 @@ from .api import (  # noqa: F401
     bvp_particle_values,
     default_context,
     forcing_basis,
+    GalerkinBasis,
+    GalerkinResult,
+    galerkin_field_grid,
+    galerkin_solve_ad,
+    galerkin_spectral_radius,
     forcing_cost,
     nelder_mead,
     optimize_forcing,

@@ -75,6 +75,15 @@ class smc_chain_outputs(C.Structure):
                 ("accepted", C.POINTER(C.c_int64)), ("phi_trace", _dp), ("samples", _dp)]
 
 
+class smc_galerkin_basis(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("cutoff", C.c_int32)]
+
+
+class smc_galerkin_result(C.Structure):
+    _fields_ = [("observation_values", _dp), ("coefficients_at_observations", _dp), ("final_coefficients", _dp),
+                ("dt_used", C.c_double), ("steps", C.c_int64)]
+
+
 class smc_stats(C.Structure):
     _fields_ = [("particle_kernel_ms", C.c_double), ("reduce_ms", C.c_double),
                 ("kernel_launches", C.c_int64), ("particle_steps", C.c_int64),
@@ -117,6 +126,13 @@ _PROTOS = {
     "smc_bvp_forcing_basis": (C.c_int, [C.c_void_p, C.POINTER(smc_bvp_problem), C.c_uint64, _dp, _dp, _dp,
                                         C.POINTER(C.c_int64)]),
     "smc_pcn_num_samples": (C.c_int64, [C.POINTER(smc_chain_config)]),
+    "smc_galerkin_n_basis": (C.c_int64, [C.POINTER(smc_galerkin_basis)]),
+    "smc_galerkin_modes": (C.c_int, [C.POINTER(smc_galerkin_basis), C.POINTER(C.c_int32)]),
+    "smc_galerkin_spectral_radius": (C.c_int, [C.c_void_p, C.POINTER(smc_ad_problem), C.POINTER(smc_galerkin_basis),
+                                               _dp]),
+    "smc_galerkin_solve_ad": (C.c_int, [C.c_void_p, C.POINTER(smc_ad_problem), C.POINTER(smc_galerkin_basis),
+                                        C.c_double, C.POINTER(smc_galerkin_result)]),
+    "smc_galerkin_field_grid": (C.c_int, [C.c_void_p, C.POINTER(smc_galerkin_basis), _dp, C.c_int32, _dp]),
     "smc_pcn_chains": (C.c_int, [C.c_void_p, C.POINTER(smc_ad_problem), C.POINTER(smc_prior), _dp, C.c_double,
                                  C.c_uint64, C.c_int64, C.POINTER(C.c_uint64), _dp, C.POINTER(smc_chain_config),
                                  C.POINTER(smc_chain_outputs)]),

@@ -8,12 +8,13 @@ forward maps and the callers above them on the B200 path.
     python -m paper_1808_10580_b200.cli optimize    --config C --out F ...
 
 Exit codes: 0 ok, 2 ConfigError ("config error: ..."), 1 any other error
-("error: ..."), argument errors as the parser reports them (2).  `reference`
-(Galerkin / FD solvers) and `benchmark` (the CPU cost-scaling harness) are not
-part of the hot path this repository rebuilds: they exit 1
-with an explanation.  `--workers` / SCALARMC_WORKERS are resolved and
-validated as in the reference (cli.cpp:40-50) and otherwise ignored: the
-device is the worker pool.
+("error: ..."), argument errors as the parser reports them (2).
+`reference --method galerkin` runs the device spectral solver; `reference
+--method fd` (finite-difference Dirichlet solver) and `benchmark` (the CPU
+cost-scaling harness) are not part of what this repository rebuilds
+(SURVEY.md §8, §2): they exit 1 with an explanation.  `--workers` /
+SCALARMC_WORKERS are resolved and validated as in the reference
+(cli.cpp:40-50) and otherwise ignored: the device is the worker pool.
 """
 from __future__ import annotations
 
@@ -141,6 +142,33 @@ def cmd_optimize(opts) -> int:
     return 0
 
 
+def cmd_reference(opts) -> int:
+    """cli.cpp:98-138, `--method galerkin` (the spectral reference solver on
+    the device; `fd` — the finite-difference Dirichlet solver — is not
+    rebuilt here)."""
+    cfg = load_config(opts.config)
+    from .config import ReferenceSection
+    ref = cfg.reference or ReferenceSection()
+    with _open_output(opts.out) as out:
+        grid_writer = RecordWriter(out, opts.format, ["x1", "x2", "value"])
+        obs_writer = RecordWriter(sys.stdout, opts.format, ["obs", "x1", "x2", "value"])
+        if opts.method == "galerkin":
+            spec = make_ad_spec(cfg)
+            dt_ref = ref.dt_ref if ref.dt_ref > 0.0 else spec.resolved_dt() / 10.0
+            result = S.galerkin_solve_ad(spec, ref.galerkin_cutoff, dt_ref)
+            n = ref.field_grid
+            field = S.galerkin_field_grid(result, n)
+            for i in range(n):
+                for j in range(n):
+                    grid_writer.write_row([i / n, j / n, field[i * n + j]])
+            for j, v in enumerate(result.observation_values):
+                o = spec.observations[j]
+                obs_writer.write_row([float(j), o.x[0], o.x[1], v])
+            return 0
+        raise RuntimeError("`reference --method fd` (finite-difference Dirichlet solver) is not part of the B200 "
+                           "path; it stays in scalarmc")
+
+
 def _not_on_path(name: str):
     def run(opts) -> int:
         raise RuntimeError(f"`{name}` is not part of the B200 forward-map path (the Galerkin/FD reference solvers "
@@ -168,7 +196,7 @@ def build_parser() -> argparse.ArgumentParser:
         run=cmd_forward_bvp)
     ref = common(sub.add_parser("reference", help="reference solver (full field + observations)"))
     ref.add_argument("--method", required=True, choices=["galerkin", "fd"])
-    ref.set_defaults(run=_not_on_path("reference"))
+    ref.set_defaults(run=cmd_reference)
     smp = common(sub.add_parser("sample", help="pCN MCMC sampling of the posterior"))
     smp.add_argument("--steps", type=int, default=-1, help="chain length override")
     smp.add_argument("--beta", type=float, default=-1.0, help="pCN step size override")

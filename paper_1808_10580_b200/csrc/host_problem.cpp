@@ -6,6 +6,7 @@
 #include "disk_shape.h"
 
 #include <algorithm>
+#include <complex>
 #include <cmath>
 #include <limits>
 
@@ -359,6 +360,122 @@ PackMap pack_map(int K, bool disk, const LatticeHost* lattice) {
         }
     }
     return m;
+}
+
+GalerkinModes galerkin_modes(const smc_galerkin_basis& b) {
+    const int L = b.cutoff;
+    if (L < 1) raise(SMC_EINVAL, "GalerkinBasis: cutoff must be >= 1");
+    if (b.kind != 0 && b.kind != 1) raise(SMC_EINVAL, "GalerkinBasis: unknown kind");
+    GalerkinModes m;
+    for (int k1 = -L; k1 <= L; ++k1)
+        for (int k2 = -L; k2 <= L; ++k2) {
+            if (b.kind == 1 && double(k1) * k1 + double(k2) * k2 > double(L) * L) continue;
+            m.k1.push_back(k1);
+            m.k2.push_back(k2);
+            m.max_abs = std::max({m.max_abs, std::abs(k1), std::abs(k2)});
+        }
+    return m;
+}
+
+std::vector<double> galerkin_assemble(double kappa, const PreparedVelocity& v, const GalerkinModes& m) {
+    using cd = std::complex<double>;
+    const double two_pi = 2.0 * 3.14159265358979323846;
+    const int64_t nb = m.size();
+    std::vector<cd> A(static_cast<size_t>(nb * nb), cd(0.0, 0.0));
+    const cd i2pi(0.0, two_pi);
+    if (v.is_constant) {
+        for (int64_t l = 0; l < nb; ++l)
+            A[static_cast<size_t>(l * nb + l)] -= i2pi * (v.c1 * double(m.k1[l]) + v.c2 * double(m.k2[l]));
+    } else {
+        // vector_coefficients (fields.cpp:112-123) on a dense (2K+1)^2 grid
+        const int K = v.K, W = 2 * K + 1;
+        std::vector<cd> c1(static_cast<size_t>(W * W)), c2(static_cast<size_t>(W * W));
+        std::vector<char> has(static_cast<size_t>(W * W), 0);
+        auto put = [&](int k1, int k2, cd a, cd b) {
+            const size_t i = static_cast<size_t>((k1 + K) * W + (k2 + K));
+            c1[i] = a;
+            c2[i] = b;
+            has[i] = 1;
+        };
+        for (const auto& md : v.modes) {
+            const double kn = std::sqrt(double(md.k1) * md.k1 + double(md.k2) * md.k2);
+            const double d1 = -double(md.k2) / kn, d2 = double(md.k1) / kn;
+            const cd c(md.re, md.im);
+            put(md.k1, md.k2, c * d1, c * d2);
+            const cd cm = -std::conj(c);
+            put(-md.k1, -md.k2, cm * (-d1), cm * (-d2));
+        }
+        for (int64_t l = 0; l < nb; ++l)
+            for (int64_t j = 0; j < nb; ++j) {
+                const int d1 = m.k1[l] - m.k1[j], d2 = m.k2[l] - m.k2[j];
+                if (d1 < -K || d1 > K || d2 < -K || d2 > K) continue;
+                const size_t i = static_cast<size_t>((d1 + K) * W + (d2 + K));
+                if (!has[i]) continue;
+                A[static_cast<size_t>(l * nb + j)] -= (c1[i] * double(m.k1[j]) + c2[i] * double(m.k2[j])) * i2pi;
+            }
+    }
+    for (int64_t l = 0; l < nb; ++l) {
+        const double ksq = two_pi * two_pi * (double(m.k1[l]) * m.k1[l] + double(m.k2[l]) * m.k2[l]);
+        A[static_cast<size_t>(l * nb + l)] -= kappa * ksq;
+    }
+    std::vector<double> out(static_cast<size_t>(2 * nb * nb));
+    for (size_t i = 0; i < A.size(); ++i) {
+        out[2 * i] = A[i].real();
+        out[2 * i + 1] = A[i].imag();
+    }
+    return out;
+}
+
+double galerkin_radius(const std::vector<double>& A, int64_t nb) {
+    double r = 0.0;
+    for (int64_t l = 0; l < nb; ++l) {
+        double s = 0.0;
+        for (int64_t j = 0; j < nb; ++j) {
+            const size_t i = static_cast<size_t>(l * nb + j);
+            s += std::hypot(A[2 * i], A[2 * i + 1]);
+        }
+        r = std::max(r, s);
+    }
+    return r;
+}
+
+bool galerkin_project_exact(const smc_scalar_field& f, const GalerkinModes& m, std::vector<double>& theta) {
+    const double two_pi = 2.0 * 3.14159265358979323846;
+    const int64_t nb = m.size();
+    theta.assign(static_cast<size_t>(2 * nb), 0.0);
+    const int L = std::max(m.max_abs, 0);
+    auto place = [&](int k1, int k2, double re, double im) {
+        if (k1 < -L || k1 > L || k2 < -L || k2 > L) return;  // outside cutoff: truncated
+        for (int64_t i = 0; i < nb; ++i)
+            if (m.k1[i] == k1 && m.k2[i] == k2) {
+                theta[2 * i] += re;
+                theta[2 * i + 1] += im;
+                return;
+            }
+    };
+    if (f.kind == SMC_SCALAR_CONSTANT) {
+        place(0, 0, f.constant, 0.0);
+        return true;
+    }
+    if (f.kind != SMC_SCALAR_COSINE) return false;
+    for (int64_t t = 0; t < f.n_terms; ++t) {
+        const double k1d = f.freq[2 * t] / two_pi, k2d = f.freq[2 * t + 1] / two_pi;
+        if (std::abs(k1d - std::round(k1d)) > 1e-12 || std::abs(k2d - std::round(k2d)) > 1e-12) return false;
+    }
+    for (int64_t t = 0; t < f.n_terms; ++t) {
+        const int k1 = static_cast<int>(std::lround(f.freq[2 * t] / two_pi));
+        const int k2 = static_cast<int>(std::lround(f.freq[2 * t + 1] / two_pi));
+        // a cos(2 pi k.x + phi) = (a/2) e^{i phi} e_k + (a/2) e^{-i phi} e_{-k}
+        const double hr = 0.5 * f.amplitude[t] * std::cos(f.phase[t]);
+        const double hi = 0.5 * f.amplitude[t] * std::sin(f.phase[t]);
+        if (k1 == 0 && k2 == 0) {
+            place(0, 0, 2.0 * hr, 0.0);
+        } else {
+            place(k1, k2, hr, hi);
+            place(-k1, -k2, hr, -hi);
+        }
+    }
+    return true;
 }
 
 AdObsImg make_ad_obs(double t, double x1, double x2, double dt, double sigma) {

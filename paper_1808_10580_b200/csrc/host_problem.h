@@ -76,6 +76,21 @@ PackMap pack_map(int cutoff, bool disk, const LatticeHost* lattice);
 PreparedVelocity prior_structure(int cutoff);
 
 // Step schedule of one AD observation (sde.cpp:42-45).
+// ---- spectral Galerkin reference solver (src/galerkin.cpp) ----------------
+struct GalerkinModes {
+    std::vector<int> k1, k2;  // basis order: k1 = -L..L outer, k2 = -L..L inner (galerkin.cpp:20-33)
+    int max_abs = 0;
+    int64_t size() const { return static_cast<int64_t>(k1.size()); }
+};
+GalerkinModes galerkin_modes(const smc_galerkin_basis& b);
+// Dense system A (galerkin.cpp:108-142), row-major, complex interleaved
+// (2 nb^2 doubles), built with the reference's complex arithmetic.
+std::vector<double> galerkin_assemble(double kappa, const PreparedVelocity& v, const GalerkinModes& m);
+double galerkin_radius(const std::vector<double>& A, int64_t nb);  // max_l sum_m |A_lm|
+// Exact projection of a constant or integer-mode cosine theta_0
+// (galerkin.cpp:43-81) into theta (2 nb doubles); false: needs quadrature.
+bool galerkin_project_exact(const smc_scalar_field& f, const GalerkinModes& m, std::vector<double>& theta);
+
 AdObsImg make_ad_obs(double t, double x1, double x2, double dt, double sigma);
 
 }  // namespace smc

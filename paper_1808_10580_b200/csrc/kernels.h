@@ -154,6 +154,16 @@ cudaError_t launch_pack(const PackDev& M, const double* Up, int64_t dim, int64_t
 cudaError_t launch_pcn_accept(const PcnStep& S, const void* est, cudaStream_t s);
 cudaError_t launch_pcn_commit(const PcnStep& S, cudaStream_t s);
 
+// Spectral Galerkin reference solver (galerkin_kernels.cu).
+cudaError_t launch_galerkin_step(const double* A, const double* th, double* out, int64_t nb, double dt,
+                                 cudaStream_t s);
+cudaError_t launch_galerkin_quadrature(const ScalarImg& f, const int* k1, const int* k2, int64_t nb, int n,
+                                       double* theta, cudaStream_t s);
+cudaError_t launch_galerkin_observe(const double* th, const int* k1, const int* k2, int64_t nb, double x1, double x2,
+                                    double* out, cudaStream_t s);
+cudaError_t launch_galerkin_field_grid(const double* c, const int* k1, const int* k2, int64_t nb, int n, double* grid,
+                                       cudaStream_t s);
+
 // Diagnostics / microbenchmarks.
 cudaError_t launch_philox(int64_t n, const uint32_t* ctr, const uint32_t* key, uint32_t* out,
                           cudaStream_t s);

@@ -252,5 +252,9 @@ def test_cli_usage_errors(tmp_path):
     assert _cli().returncode == 2
     assert _cli("forward-ad", "--config", "x.json").returncode == 2  # --out required
     assert _cli("forward-ad", "--config", "x", "--out", "y", "--format", "xml").returncode == 2
-    r = _cli("reference", "--config", "x", "--out", "y", "--method", "fd")
+    r = _cli("benchmark", "--config", "x", "--out", "y")
     assert r.returncode == 1 and "not part of the B200 forward-map path" in r.stderr
+    p = tmp_path / "bvp.json"
+    p.write_text(json.dumps(BVP))
+    r = _cli("reference", "--config", p, "--out", tmp_path / "g.csv", "--method", "fd")
+    assert r.returncode == 1 and "finite-difference" in r.stderr

@@ -128,3 +128,30 @@ def test_optimize(tmp_path):
         assert g[0] == w[0]
         assert close(g[1], w[1], 1e-8, 1e-6)
         assert np.allclose(np.array(g[2:], float), np.array(w[2:], float), rtol=1e-8, atol=1e-10)
+
+
+def test_reference_galerkin(tmp_path):
+    """`reference --method galerkin` (cli.cpp:98-122): grid file + observation
+    rows on stdout, against the numpy restatement of galerkin.cpp."""
+    from oracle import galerkin_oracle as G
+    from paper_1808_10580_b200.config import load_config, make_ad_spec
+    from paper_1808_10580_b200.records import format_double
+    cfg_path = tmp_path / "gal.json"
+    cfg = json.loads((GOLD / "ad.json").read_text())
+    cfg["reference"] = {"galerkin_cutoff": 5, "dt_ref": 2.5e-4, "field_grid": 9}
+    cfg_path.write_text(json.dumps(cfg))
+    r = cli("reference", "--config", cfg_path, "--out", tmp_path / "grid.csv", "--method", "galerkin")
+    assert r.returncode == 0, r.stderr
+    spec = make_ad_spec(load_config(str(cfg_path)))
+    vals, theta, steps, modes = G.solve(spec, "box", 5, 2.5e-4)
+    gh, gr = read_csv(tmp_path / "grid.csv")
+    assert gh == ["x1", "x2", "value"] and len(gr) == 81
+    want = G.field_grid(theta, modes, 9)
+    for q, row in enumerate(gr):
+        assert row[0] == format_double((q // 9) / 9) and row[1] == format_double((q % 9) / 9)
+        assert abs(float(row[2]) - want[q]) < 1e-10
+    lines = r.stdout.splitlines()
+    assert lines[0] == "obs,x1,x2,value" and len(lines) == 1 + len(vals)
+    for j, line in enumerate(lines[1:]):
+        f = line.split(",")
+        assert f[0] == str(j) and abs(float(f[3]) - vals[j]) < 1e-10 * max(1.0, abs(vals[j]))
