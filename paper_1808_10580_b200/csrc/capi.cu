@@ -829,25 +829,39 @@ smc_status smc_galerkin_solve_ad(smc_ctx* ctx, const smc_ad_problem* prob, const
         if (!(dt_ref > 0.0)) raise(SMC_EINVAL, "galerkin_solve_ad: dt_ref must be positive");
         const GalerkinModes m = galerkin_modes(*basis);
         const int64_t nb = m.size();
-        const std::vector<double> A = galerkin_assemble(p.kappa, v, m);
-        // explicit-Euler stability estimate (galerkin.cpp:170-177)
-        const double radius = galerkin_radius(A, nb);
+        cudaStream_t s = ctx->stream;
+        double* dA = ctx->gal_A.get<double>(static_cast<size_t>(2 * nb * nb));
+        double* th[2] = {ctx->gal_t0.get<double>(static_cast<size_t>(2 * nb)),
+                         ctx->gal_t1.get<double>(static_cast<size_t>(2 * nb))};
+        int* dk1 = ctx->gal_k1.get<int>(static_cast<size_t>(nb));
+        int* dk2 = ctx->gal_k2.get<int>(static_cast<size_t>(nb));
+        double* dobs = ctx->gal_obs.get<double>(static_cast<size_t>(std::max<int64_t>(p.n_obs, 1)));
+        CK(cudaMemcpyAsync(dk1, m.k1.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(dk2, m.k2.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, s));
+        // A assembled on the device (bit-identical to the host restatement of
+        // galerkin.cpp:108-142), then the explicit-Euler stability estimate
+        // (galerkin.cpp:170-177)
+        const VhatGrid vg = galerkin_vhat_grid(v);
+        const size_t cells = vg.present.size();
+        double* dvh = ctx->gal_grid.get<double>(4 * cells + (cells + 7) / 8 + 1);
+        auto* dpres = reinterpret_cast<unsigned char*>(dvh + 4 * cells);
+        auto* dradius = ctx->tmp_a.get<unsigned long long>(1);
+        CK(cudaMemcpyAsync(dvh, vg.c.data(), sizeof(double) * 4 * cells, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(dpres, vg.present.data(), cells, cudaMemcpyHostToDevice, s));
+        CK(launch_galerkin_assemble(dvh, dpres, vg.K, dk1, dk2, nb, p.kappa, v.is_constant ? 1 : 0, v.c1, v.c2, dA,
+                                    dradius, s));
+        count_launches(ctx, 2);
+        unsigned long long rbits = 0;
+        CK(cudaMemcpyAsync(&rbits, dradius, sizeof(rbits), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        double radius;
+        std::memcpy(&radius, &rbits, sizeof(radius));
         if (radius * dt_ref >= 2.0) {
             std::ostringstream msg;
             msg << "galerkin_solve_ad: dt_ref " << dt_ref << " violates the stability estimate; suggest dt_ref <= "
                 << 1.8 / radius;
             raise(SMC_ERUNTIME, msg.str());
         }
-        cudaStream_t s = ctx->stream;
-        double* dA = ctx->gal_A.get<double>(A.size());
-        double* th[2] = {ctx->gal_t0.get<double>(static_cast<size_t>(2 * nb)),
-                         ctx->gal_t1.get<double>(static_cast<size_t>(2 * nb))};
-        int* dk1 = ctx->gal_k1.get<int>(static_cast<size_t>(nb));
-        int* dk2 = ctx->gal_k2.get<int>(static_cast<size_t>(nb));
-        double* dobs = ctx->gal_obs.get<double>(static_cast<size_t>(std::max<int64_t>(p.n_obs, 1)));
-        CK(cudaMemcpyAsync(dA, A.data(), sizeof(double) * A.size(), cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(dk1, m.k1.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(dk2, m.k2.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, s));
         // projection of theta_0 (galerkin.cpp:43-101)
         std::vector<double> theta0;
         if (galerkin_project_exact(p.initial_condition, m, theta0)) {

@@ -426,6 +426,33 @@ std::vector<double> galerkin_assemble(double kappa, const PreparedVelocity& v, c
     return out;
 }
 
+VhatGrid galerkin_vhat_grid(const PreparedVelocity& v) {
+    using cd = std::complex<double>;
+    VhatGrid g;
+    g.K = v.is_constant ? 0 : v.K;
+    const int W = 2 * g.K + 1;
+    g.c.assign(static_cast<size_t>(4 * W * W), 0.0);
+    g.present.assign(static_cast<size_t>(W * W), 0);
+    if (v.is_constant) return g;
+    auto put = [&](int k1, int k2, cd a, cd b) {
+        const size_t i = static_cast<size_t>((k1 + g.K) * W + (k2 + g.K));
+        g.c[4 * i] = a.real();
+        g.c[4 * i + 1] = a.imag();
+        g.c[4 * i + 2] = b.real();
+        g.c[4 * i + 3] = b.imag();
+        g.present[i] = 1;
+    };
+    for (const auto& md : v.modes) {
+        const double kn = std::sqrt(double(md.k1) * md.k1 + double(md.k2) * md.k2);
+        const double d1 = -double(md.k2) / kn, d2 = double(md.k1) / kn;
+        const cd c(md.re, md.im);
+        put(md.k1, md.k2, c * d1, c * d2);
+        const cd cm = -std::conj(c);
+        put(-md.k1, -md.k2, cm * (-d1), cm * (-d2));
+    }
+    return g;
+}
+
 double galerkin_radius(const std::vector<double>& A, int64_t nb) {
     double r = 0.0;
     for (int64_t l = 0; l < nb; ++l) {

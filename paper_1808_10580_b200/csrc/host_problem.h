@@ -87,6 +87,14 @@ GalerkinModes galerkin_modes(const smc_galerkin_basis& b);
 // (2 nb^2 doubles), built with the reference's complex arithmetic.
 std::vector<double> galerkin_assemble(double kappa, const PreparedVelocity& v, const GalerkinModes& m);
 double galerkin_radius(const std::vector<double>& A, int64_t nb);  // max_l sum_m |A_lm|
+// vector_coefficients (fields.cpp:112-123) on a dense (2K+1)^2 grid for the
+// device assembly: 4 doubles per cell [c1re, c1im, c2re, c2im] + present flags.
+struct VhatGrid {
+    int K = 0;
+    std::vector<double> c;
+    std::vector<unsigned char> present;
+};
+VhatGrid galerkin_vhat_grid(const PreparedVelocity& v);
 // Exact projection of a constant or integer-mode cosine theta_0
 // (galerkin.cpp:43-81) into theta (2 nb doubles); false: needs quadrature.
 bool galerkin_project_exact(const smc_scalar_field& f, const GalerkinModes& m, std::vector<double>& theta);

@@ -157,6 +157,9 @@ cudaError_t launch_pcn_commit(const PcnStep& S, cudaStream_t s);
 // Spectral Galerkin reference solver (galerkin_kernels.cu).
 cudaError_t launch_galerkin_step(const double* A, const double* th, double* out, int64_t nb, double dt,
                                  cudaStream_t s);
+cudaError_t launch_galerkin_assemble(const double* vhat, const unsigned char* present, int K, const int* k1,
+                                     const int* k2, int64_t nb, double kappa, int constant, double v1, double v2,
+                                     double* A, unsigned long long* radius_bits, cudaStream_t s);
 cudaError_t launch_galerkin_quadrature(const ScalarImg& f, const int* k1, const int* k2, int64_t nb, int n,
                                        double* theta, cudaStream_t s);
 cudaError_t launch_galerkin_observe(const double* th, const int* k1, const int* k2, int64_t nb, double x1, double x2,

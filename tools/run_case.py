@@ -73,6 +73,26 @@ if args.config in ("pcn", "pcn8"):
           f"{B * n_steps / el:.4g} chain-steps/s ({el / n_steps * 1e6:.1f} us/step), "
           f"acceptance {res['acceptance_rate'].mean():.3f}")
     sys.exit(0)
+if args.config == "galerkin":
+    # the paper's Fig. 8 reference solve: C2's velocity, box cutoff L (default
+    # 16: 1089 modes, A = 19 MB), dt_ref from the stability estimate, t = 1
+    import math
+    import time
+    import numpy as np
+    import specs
+    L = args.cutoff or 16
+    u = S.prior_draw(specs.C2_PRIOR, 808, 0xBE9C4, 0, ctx)
+    spec = specs.c2_spec(u, n_particles=1000)
+    radius = S.galerkin_spectral_radius(spec, L, ctx)
+    dt = 1.0 / radius
+    for rep in range(max(args.reps, 1)):
+        t0 = time.perf_counter()
+        res = S.galerkin_solve_ad(spec, L, dt, ctx=ctx)
+        el = time.perf_counter() - t0
+    nb = len(res.basis_modes)
+    print(f"galerkin L={L} nb={nb} dt={dt:.3g} steps={res.steps}: {el * 1e3:.1f} ms -> {el / res.steps * 1e6:.2f} us/step, "
+          f"{16.0 * nb * nb * res.steps / el / 1e12:.2f} TB/s of A streamed; obs[0]={res.observation_values[0]:.12g}")
+    sys.exit(0)
 if args.config in ("c3", "c3b"):
     # paper BVP, F=(1,-0.5,2), 25 obs, 1e6 walkers/obs, seed 606
     import specs
