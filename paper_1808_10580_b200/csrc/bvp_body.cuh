@@ -22,6 +22,7 @@
 #include "scalar_eval.cuh"
 #include "smc_device.cuh"
 #include "velocity.cuh"
+#include "disk_velocity.cuh"
 
 namespace smc {
 
@@ -79,9 +80,18 @@ struct Forcing {
 // unit-bump integrals I_j = int phi_j(X_t) dt and store value = bc(X_tau), so
 // G(F) = E[bc] - sum_j F_j E[I_j] for every amplitude vector F from one pass
 // (common random numbers: the paths do not depend on F).
-template <class T, bool STRICT, int KCAP, int NB = 0, int VEL = 0, bool BASIS = false>
+// DISK_K > 0 (FP64, Fourier velocity filling the disk |k| <= DISK_K): the
+// compile-time disk series of K1 (disk_velocity.cuh) from a coefficient block
+// staged in shared memory, instead of the runtime-tiled lattice loop.
+template <class T, bool STRICT, int KCAP, int NB = 0, int VEL = 0, bool BASIS = false, int DISK_K = 0>
 __global__ void __launch_bounds__(kBvpBlock) bvp_walkers(const BvpLaunch L) {
     constexpr unsigned FULL = 0xffffffffu;
+    __shared__ __align__(16) T disk_coef[DISK_K > 0 ? DiskShape<DISK_K>::n_coef : 2];
+    if constexpr (DISK_K > 0) {
+        for (int i = threadIdx.x; i < DiskShape<DISK_K>::n_coef; i += blockDim.x) disk_coef[i] = T(L.disk_coef[i]);
+        __syncthreads();
+    }
+    const disk::SmemCoef<T> dc{static_cast<uint32_t>(__cvta_generic_to_shared(disk_coef))};
     const int lane = threadIdx.x & 31;
     const unsigned long long total = static_cast<unsigned long long>(L.n_obs) * L.n_particles;
     const uint32_t k0 = static_cast<uint32_t>(L.seed), k1 = static_cast<uint32_t>(L.seed >> 32);
@@ -145,6 +155,12 @@ __global__ void __launch_bounds__(kBvpBlock) bvp_walkers(const BvpLaunch L) {
                 if (VEL == 1 || L.vel.is_constant) {
                     v1 = T(L.vel.c1);
                     v2 = T(L.vel.c2);
+                } else if constexpr (VEL == 0 && DISK_K > 0) {
+                    const T xa[1] = {x1}, xb[1] = {x2};
+                    T va[1], vb[1];
+                    disk::velocity_disk<DISK_K, T, 1>(dc, xa, xb, va, vb);
+                    v1 = va[0];
+                    v2 = vb[0];
                 } else if constexpr (VEL == 0) {
                     velocity_lattice<T, double>(lat, lat.coef, x1, x2, v1, v2);
                 }

@@ -43,6 +43,7 @@ cudaError_t launch_bvp_walkers(const BvpLaunch& L, int n_sms, cudaStream_t s) {
     // keeps its parameters in registers; a constant velocity compiles the
     // Fourier series out.
     const int nb = (L.forcing.kind == SMC_SCALAR_BUMPS && L.forcing.n >= 1 && L.forcing.n <= 4) ? L.forcing.n : 0;
+    if (L.disk_K > 0 && L.precision == SMC_FP64 && !L.vel.is_constant) return launch_bvp_disk(L, blocks, s);
     if (L.precision == SMC_FP32) dispatch<float>(L, nb, blocks, s);
     else dispatch<double>(L, nb, blocks, s);
     return cudaGetLastError();

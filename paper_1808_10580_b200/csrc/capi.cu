@@ -397,8 +397,21 @@ BvpLaunch prepare_bvp(smc_ctx* ctx, const smc_bvp_problem& p, int64_t obs_begin,
     const ScalarRef fr = add_scalar(im, p.forcing);
     const ScalarRef br = add_scalar(im, p.boundary_data);
     const VelRef vr = add_velocity(im, v, {&v});
+    // dense Fourier fields on |k| <= 12: the compile-time disk series (as K1)
+    const bool disk = !v.is_constant && p.precision == SMC_FP64 && v.K <= kDiskMaxK &&
+                      2 * v.modes.size() >= static_cast<size_t>(disk_n_modes(v.K)) &&
+                      std::getenv("SMC_DISABLE_DISK") == nullptr;
+    size_t disk_off = 0;
+    if (disk) {
+        disk_off = im.reserve(static_cast<size_t>(disk_n_coef(v.K)) * sizeof(double));
+        disk_fill(v.K, v, reinterpret_cast<double*>(im.bytes.data() + disk_off));
+    }
     unsigned char* base = ctx->upload(im);
     BvpLaunch L{};
+    if (disk) {
+        L.disk_K = v.K;
+        L.disk_coef = reinterpret_cast<const double*>(base + disk_off);
+    }
     L.vel = patch(vr, base);
     L.forcing = patch(fr, base);
     L.boundary = patch(br, base);

@@ -65,10 +65,15 @@ struct BvpLaunch {
     double* aux;               // exit time
     uint8_t* failed;
     double* basis;             // forcing-basis mode: [n_bumps][n_obs][n_particles] unit-bump integrals
+    const double* disk_coef;   // disk_shape.h coefficient block when disk_K > 0
+    int32_t disk_K;            // > 0: dense Fourier velocity on |k| <= disk_K (FP64 walkers use bvp_disk.cu)
+    int32_t pad2_;
 };
 
 cudaError_t launch_bvp_walkers(const BvpLaunch& L, int n_sms, cudaStream_t s);
 cudaError_t launch_bvp_walkers_strict(const BvpLaunch& L, int n_sms, cudaStream_t s);
+// FP64 walkers with the compile-time disk velocity (L.disk_K in 1..kDiskMaxK).
+cudaError_t launch_bvp_disk(const BvpLaunch& L, unsigned blocks, cudaStream_t s);
 // Forcing-basis mode (Gaussian-bump forcing with 1..4 terms, FP64).
 cudaError_t launch_bvp_basis(const BvpLaunch& L, int n_sms, cudaStream_t s);
 

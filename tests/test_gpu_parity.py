@@ -387,3 +387,19 @@ def test_batched_non_finite_coefficient_rejected(ctx):
         S.observe_ad_batched(specs.c4_base(n_particles=64), prior, U, 1, ctx=ctx)
     U[2, 5] = 0.0
     S.observe_ad_batched(specs.c4_base(n_particles=64), prior, U, 1, ctx=ctx)  # context still usable
+
+
+@pytest.mark.parametrize("disk_velocity", [True, False])
+def test_bvp_dense_fourier_velocity_matches_oracle(ctx, port, monkeypatch, disk_velocity):
+    """C3b: the paper BVP with C2's K=8 prior-draw velocity.
+    A dense field takes the walkers with the compile-time disk series
+    (bvp_disk.cu); SMC_DISABLE_DISK forces the tiled lattice walkers."""
+    if not disk_velocity:
+        monkeypatch.setenv("SMC_DISABLE_DISK", "1")
+    spec = specs.c3_spec(n_particles=400)
+    spec.observations = spec.observations[:3]
+    u = S.prior_draw(specs.C2_PRIOR, 808, 0xBE9C4, 0, ctx)
+    spec.velocity = S.VelocityField.fourier(S.velocity_from_coefficients(specs.C2_PRIOR, u))
+    got = S.observe_bvp(spec, 606, ctx=ctx)
+    want = port.observe_bvp(spec, 606)
+    assert_estimates(got, list(want), 1.0)
