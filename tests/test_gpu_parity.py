@@ -403,3 +403,35 @@ def test_bvp_dense_fourier_velocity_matches_oracle(ctx, port, monkeypatch, disk_
     got = S.observe_bvp(spec, 606, ctx=ctx)
     want = port.observe_bvp(spec, 606)
     assert_estimates(got, list(want), 1.0)
+
+
+@pytest.mark.parametrize("n", [2, 3, 1023, 1024, 1025, 4097])
+def test_ragged_particle_counts(ctx, port, n):
+    """Chunk boundaries of K3 (1024-leaf chunks, -0.0 padding): the estimate
+    is the reference's pairwise reduction of the kernel's own per-particle
+    values, bit for bit, and the particles are the oracle's."""
+    spec = specs.c1_two_mode(n_particles=n)
+    est = S.observe_ad(spec, 7, ctx=ctx)
+    for j in range(len(spec.observations)):
+        vals = S.ad_particle_values(spec, j, 7, n, ctx)
+        mean = port.pairwise_sum(vals) / n
+        var = port.pairwise_sum((vals - mean) ** 2) / (n - 1)
+        assert est[j].mean == mean and est[j].std_error == math.sqrt(var / n)
+        assert est[j].n_particles == n and est[j].n_failed == 0
+        assert np.max(np.abs(vals - port.ad_particle_values(spec, j, 7, n))) < 1e-12
+
+
+@pytest.mark.parametrize("n", [2, 5, 1025])
+def test_bvp_ragged_with_failures(ctx, port, n):
+    """max_steps failures excluded before the tree (executor.cpp:93-101) at
+    ragged walker counts."""
+    spec = specs.paper_bvp(n_particles=n, observations=[(0.94, 0.94), (0.5, 0.5)])
+    spec.max_steps = 60
+    try:
+        want = port.observe_bvp(spec, 606)
+    except RuntimeError:
+        with pytest.raises(RuntimeError):
+            S.observe_bvp(spec, 606, ctx=ctx)
+        return
+    got = S.observe_bvp(spec, 606, ctx=ctx)
+    assert_estimates(got, list(want), 1.0)
