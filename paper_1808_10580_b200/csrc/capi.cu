@@ -7,158 +7,22 @@
 // particle kernel -> K3 tree reduction passes -> estimates kernel -> one D2H
 // copy of n_obs x 40 B.  All on the context's stream; persistent buffers grow
 // and are reused across calls.
-#include <cuda_runtime.h>
-
-#include <algorithm>
-#include <cmath>
-#include <cstdlib>
-#include <sstream>
-#include <cstring>
-#include <new>
-#include <string>
-#include <vector>
-
-#include "../../include/scalarmc_b200.h"
-#include "disk_shape.h"
-#include "host_problem.h"
-#include "kernels.h"
-
-namespace {
-constexpr int kLatticeTileHost = 8;  // == kLatticeTile (velocity.cuh) / kTileW (host_problem.cpp)
-}
+#include "capi_internal.h"
 
 using namespace smc;
+using namespace smc::capi;
 
-namespace {
+namespace smc::capi {
 
 thread_local std::string g_err;
 
-#define CK(x)                                                                                       \
-    do {                                                                                            \
-        cudaError_t e_ = (x);                                                                       \
-        if (e_ != cudaSuccess) raise(SMC_ECUDA, std::string("CUDA error: ") + cudaGetErrorString(e_) + \
-                                                    " (" #x ")");                                   \
-    } while (0)
-
-template <class F>
-smc_status guarded(F&& f) {
-    try {
-        f();
-        return SMC_OK;
-    } catch (const Error& e) {
-        g_err = e.msg;
-        return static_cast<smc_status>(e.code);
-    } catch (const std::bad_alloc&) {
-        g_err = "host allocation failed";
-        return SMC_ERUNTIME;
-    } catch (const std::exception& e) {
-        g_err = e.what();
-        return SMC_ERUNTIME;
-    }
-}
-
-struct DevBuf {
-    void* p = nullptr;
-    size_t cap = 0;
-    template <class T>
-    T* get(size_t n) {
-        const size_t bytes = std::max<size_t>(n * sizeof(T), 16);
-        if (bytes > cap) {
-            if (p) cudaFree(p);
-            p = nullptr;
-            cap = 0;
-            CK(cudaMalloc(&p, bytes));
-            cap = bytes;
-        }
-        return static_cast<T*>(p);
-    }
-    void release() {
-        if (p) cudaFree(p);
-        p = nullptr;
-        cap = 0;
-    }
-};
-
-struct PinnedBuf {
-    void* p = nullptr;
-    size_t cap = 0;
-    template <class T>
-    T* get(size_t n) {
-        const size_t bytes = std::max<size_t>(n * sizeof(T), 16);
-        if (bytes > cap) {
-            if (p) cudaFreeHost(p);
-            p = nullptr;
-            cap = 0;
-            CK(cudaMallocHost(&p, bytes));
-            cap = bytes;
-        }
-        return static_cast<T*>(p);
-    }
-    void release() {
-        if (p) cudaFreeHost(p);
-        p = nullptr;
-        cap = 0;
-    }
-};
-
-// Host-side image under construction: 16-byte aligned blobs in one arena.
-struct Image {
-    std::vector<unsigned char> bytes;
-    size_t add(const void* src, size_t n) {
-        const size_t off = (bytes.size() + 15) & ~size_t(15);
-        bytes.resize(off + std::max<size_t>(n, 1));
-        if (n) std::memcpy(bytes.data() + off, src, n);
-        return off;
-    }
-    template <class T>
-    size_t add_vec(const std::vector<T>& v) {
-        return add(v.data(), v.size() * sizeof(T));
-    }
-    size_t reserve(size_t n) {
-        const size_t off = (bytes.size() + 15) & ~size_t(15);
-        bytes.resize(off + std::max<size_t>(n, 1));
-        return off;
-    }
-};
-
-}  // namespace
-
-struct smc_ctx {
-    int device = 0;
-    cudaStream_t stream = nullptr;      // stream every launch goes to
-    cudaStream_t own_stream = nullptr;  // the context's own stream
-    int64_t total_launches = 0;
-    cudaEvent_t ev[4] = {};
-    DevBuf image, values, aux, flags, flags2, scratch, sums, means, sumsq, sumaux, est, counts, tmp_a, tmp_b, tmp_c;
-    DevBuf pk_ip, pk_im, pk_kp, pk_km, pk_ms, pk_u, pk_blocks, pk_bad;  // device u -> field packing
-    DevBuf gal_A, gal_t0, gal_t1, gal_k1, gal_k2, gal_obs, gal_grid;  // Galerkin reference solver
-    PinnedBuf staging, est_host;
-    smc_stats stats{};
-    // sharded AD state (smc_ad_shard_*)
-    int64_t shard_n_obs = 0, shard_span = 0;
-
-    unsigned char* upload(const Image& img) {
-        unsigned char* h = staging.get<unsigned char>(img.bytes.size());
-        std::memcpy(h, img.bytes.data(), img.bytes.size());
-        unsigned char* d = image.get<unsigned char>(img.bytes.size());
-        CK(cudaMemcpyAsync(d, h, img.bytes.size(), cudaMemcpyHostToDevice, stream));
-        return d;
-    }
-};
-
-namespace {
 
 void count_launches(smc_ctx* ctx, int64_t n) {
     ctx->stats.kernel_launches += n;
     ctx->total_launches += n;
 }
 
-// ScalarField image: term arrays appended to the image; pointers patched
-// after upload.
-struct ScalarRef {
-    ScalarImg img{};
-    size_t amp = 0, freq = 0, phase = 0, center = 0;
-};
+
 
 ScalarRef add_scalar(Image& im, const smc_scalar_field& f) {
     check_scalar(f);
@@ -192,10 +56,7 @@ ScalarImg patch(const ScalarRef& r, unsigned char* base) {
     return s;
 }
 
-struct VelRef {
-    VelImg img{};
-    size_t modes = 0, tiles = 0, coefs = 0;
-};
+
 
 // Velocity image: strict mode list + tiled lattice structure + one
 // coefficient block per sample (fills[i] for sample i).
@@ -239,14 +100,7 @@ VelImg patch(const VelRef& r, unsigned char* base) {
     return v;
 }
 
-// Everything a K1 launch needs, prepared and uploaded.
-struct AdPrepared {
-    AdLaunch L{};
-    int disk_K = 0;                  // > 0: use the compile-time disk kernel
-    const double* disk = nullptr;    // its coefficient blocks (device, one per sample)
-    int64_t n_obs = 0;
-    int64_t steps_per_particle_sum = 0;  // sum_j n_j
-};
+
 
 void check_particle_range(int64_t n_particles) {
     // Stream keys carry the particle index in 32 bits (rng.cpp:46-47); the
@@ -300,7 +154,7 @@ AdPrepared prepare_ad(smc_ctx* ctx, const smc_ad_problem& p, const std::vector<c
     return out;
 }
 
-void run_particles(smc_ctx* ctx, AdLaunch& L, const AdPrepared* P = nullptr, int64_t sample0 = 0) {
+void run_particles(smc_ctx* ctx, AdLaunch& L, const AdPrepared* P, int64_t sample0) {
     if (P && P->disk_K > 0) {
         CK(launch_ad_disk(L, P->disk_K, P->disk + sample0 * disk_n_coef(P->disk_K), ctx->stream));
     } else if (L.precision == SMC_FP64_STRICT) {
@@ -463,10 +317,7 @@ void run_bvp(smc_ctx* ctx, BvpLaunch& L, int64_t n_obs, int64_t n) {
     CK(cudaEventRecord(ctx->ev[1], s));
 }
 
-}  // namespace
 
-namespace smc {
-namespace {
 // Upload a PackMap into the context's pack buffers (reused across calls).
 PackDev upload_pack_map(smc_ctx* ctx, const PackMap& m) {
     const size_t n = static_cast<size_t>(m.stride);
@@ -482,8 +333,8 @@ PackDev upload_pack_map(smc_ctx* ctx, const PackMap& m) {
     CK(cudaMemcpyAsync(ms, m.ms.data(), n, cudaMemcpyHostToDevice, ctx->stream));
     return PackDev{m.stride, ip, im, kp, km, ms};
 }
-}  // namespace
-}  // namespace smc
+
+}  // namespace smc::capi
 
 extern "C" {
 
@@ -598,79 +449,6 @@ smc_status smc_ad_observe_single(smc_ctx* ctx, const smc_ad_problem* p, uint64_t
         if (obs_index >= static_cast<uint64_t>(p->n_obs))
             raise(SMC_ERANGE, "observe_ad_single: observation index out of range");
         ad_observe_range(ctx, *p, seed, static_cast<int64_t>(obs_index), 1, out);
-    });
-}
-
-smc_status smc_ad_observe_batched(smc_ctx* ctx, const smc_ad_problem* base, const smc_prior* prior,
-                                  int64_t n_samples, const double* u, const uint64_t* seeds, uint64_t seed,
-                                  smc_estimate* out) {
-    return guarded([&] {
-        CK(cudaSetDevice(ctx->device));
-        if (n_samples < 1) raise(SMC_EINVAL, "observe_ad_batched: need at least one sample");
-        if (prior->cutoff <= 0) raise(SMC_EINVAL, "FourierVelocityField: max_wavenumber must be positive");
-        smc_ad_problem p = *base;
-        p.velocity.is_constant = 0;
-        p.velocity.max_wavenumber = prior->cutoff;
-        check_kappa(p.kappa);
-        check_scalar(p.initial_condition);
-        // validate() without the velocity slot
-        ad_validate(p);
-        check_particle_range(p.n_particles);
-        if (p.precision == SMC_FP64_STRICT) raise(SMC_EINVAL, "strict precision is single-sample only");
-        ctx->stats = smc_stats{};
-        const int64_t n = p.n_particles, n_obs = p.n_obs;
-        // One FourierVelocityField per sample from u in prior order
-        // (velocity_from_coefficients, inference.cpp:63-73), built on the
-        // device: the image carries the full prior disk's structure and the
-        // pack kernel writes every sample's coefficient block from u.
-        const PreparedVelocity structure = prior_structure(prior->cutoff);
-        const int64_t dim = 2 * static_cast<int64_t>(structure.modes.size());
-        AdPrepared P = prepare_ad(ctx, p, {&structure}, structure, 0, n_obs);
-        const LatticeHost Lh = lattice_structure(structure);
-        const PackMap pmap = pack_map(prior->cutoff, P.disk_K > 0, &Lh);
-        const PackDev pdev = upload_pack_map(ctx, pmap);
-        double* d_u = ctx->pk_u.get<double>(static_cast<size_t>(n_samples * dim));
-        CK(cudaMemcpyAsync(d_u, u, sizeof(double) * n_samples * dim, cudaMemcpyHostToDevice, ctx->stream));
-        double* blocks = ctx->pk_blocks.get<double>(static_cast<size_t>(n_samples * pmap.stride));
-        int* d_bad = ctx->pk_bad.get<int>(1);
-        CK(cudaMemsetAsync(d_bad, 0, sizeof(int), ctx->stream));
-        for (int64_t b0 = 0; b0 < n_samples; b0 += 65535)
-            CK(launch_pack(pdev, d_u + b0 * dim, dim, std::min<int64_t>(65535, n_samples - b0),
-                           blocks + b0 * pmap.stride, d_bad, ctx->stream));
-        count_launches(ctx, (n_samples + 65534) / 65535);
-        // the FourierVelocityField ctor throws before any particle work (fields.cpp:46-47)
-        int bad = 0;
-        CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
-        if (bad) raise(SMC_EINVAL, "FourierVelocityField: non-finite coefficient");
-        if (P.disk_K > 0) {
-            P.disk = blocks;
-        } else {
-            P.L.vel.lat.coef = blocks;
-            P.L.vel.lat.sample_stride = pmap.stride;
-        }
-        uint64_t* d_seeds = nullptr;
-        if (seeds) {
-            d_seeds = ctx->tmp_a.get<uint64_t>(static_cast<size_t>(n_samples));
-            CK(cudaMemcpyAsync(d_seeds, seeds, sizeof(uint64_t) * n_samples, cudaMemcpyHostToDevice, ctx->stream));
-        }
-        double* values = ctx->values.get<double>(static_cast<size_t>(n_samples * n_obs * n));
-        CK(cudaEventRecord(ctx->ev[0], ctx->stream));
-        constexpr int64_t kMaxZ = 65535;
-        for (int64_t b0 = 0; b0 < n_samples; b0 += kMaxZ) {
-            const int64_t nb = std::min(kMaxZ, n_samples - b0);
-            AdLaunch L = P.L;
-            L.seed = seed;
-            L.seeds = d_seeds ? d_seeds + b0 : nullptr;
-            L.n_samples = static_cast<int32_t>(nb);
-            if (!L.vel.is_constant) L.vel.lat.coef += b0 * L.vel.lat.sample_stride;
-            L.values = values + b0 * n_obs * n;
-            run_particles(ctx, L, &P, b0);
-        }
-        CK(cudaEventRecord(ctx->ev[1], ctx->stream));
-        reduce_ad(ctx, values, n, n_samples * n_obs, out);
-        finish_stats(ctx);
-        ctx->stats.particle_steps = P.steps_per_particle_sum * n * n_samples;
     });
 }
 
@@ -793,198 +571,6 @@ smc_status smc_last_stats(smc_ctx* ctx, smc_stats* out) {
     });
 }
 
-// ---- spectral Galerkin reference solver (src/galerkin.cpp) ----------------
-namespace {
-// check_galerkin_inputs (galerkin.cpp:144-149): the spec's own validation
-// (isotropic diffusion is the only kind the ABI carries).
-PreparedVelocity galerkin_check_inputs(const smc_ad_problem& p) {
-    PreparedVelocity v = prepare_velocity(p.velocity);
-    check_kappa(p.kappa);
-    check_scalar(p.initial_condition);
-    ad_validate(p);
-    return v;
-}
-}  // namespace
-
-int64_t smc_galerkin_n_basis(const smc_galerkin_basis* basis) {
-    try {
-        return galerkin_modes(*basis).size();
-    } catch (...) {
-        return -1;
-    }
-}
-
-smc_status smc_galerkin_modes(const smc_galerkin_basis* basis, int32_t* modes) {
-    return guarded([&] {
-        const GalerkinModes m = galerkin_modes(*basis);
-        for (int64_t i = 0; i < m.size(); ++i) {
-            modes[2 * i] = m.k1[static_cast<size_t>(i)];
-            modes[2 * i + 1] = m.k2[static_cast<size_t>(i)];
-        }
-    });
-}
-
-smc_status smc_galerkin_spectral_radius(smc_ctx*, const smc_ad_problem* prob, const smc_galerkin_basis* basis,
-                                        double* out) {
-    return guarded([&] {
-        const PreparedVelocity v = galerkin_check_inputs(*prob);
-        const GalerkinModes m = galerkin_modes(*basis);
-        *out = galerkin_radius(galerkin_assemble(prob->kappa, v, m), m.size());
-    });
-}
-
-smc_status smc_galerkin_solve_ad(smc_ctx* ctx, const smc_ad_problem* prob, const smc_galerkin_basis* basis,
-                                 double dt_ref, smc_galerkin_result* out) {
-    return guarded([&] {
-        CK(cudaSetDevice(ctx->device));
-        const smc_ad_problem& p = *prob;
-        const PreparedVelocity v = galerkin_check_inputs(p);
-        if (!(dt_ref > 0.0)) raise(SMC_EINVAL, "galerkin_solve_ad: dt_ref must be positive");
-        const GalerkinModes m = galerkin_modes(*basis);
-        const int64_t nb = m.size();
-        cudaStream_t s = ctx->stream;
-        double* dA = ctx->gal_A.get<double>(static_cast<size_t>(2 * nb * nb));
-        double* th[2] = {ctx->gal_t0.get<double>(static_cast<size_t>(2 * nb)),
-                         ctx->gal_t1.get<double>(static_cast<size_t>(2 * nb))};
-        int* dk1 = ctx->gal_k1.get<int>(static_cast<size_t>(nb));
-        int* dk2 = ctx->gal_k2.get<int>(static_cast<size_t>(nb));
-        double* dobs = ctx->gal_obs.get<double>(static_cast<size_t>(std::max<int64_t>(p.n_obs, 1)));
-        CK(cudaMemcpyAsync(dk1, m.k1.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(dk2, m.k2.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, s));
-        // A assembled on the device (bit-identical to the host restatement of
-        // galerkin.cpp:108-142), then the explicit-Euler stability estimate
-        // (galerkin.cpp:170-177)
-        const VhatGrid vg = galerkin_vhat_grid(v);
-        const size_t cells = vg.present.size();
-        double* dvh = ctx->gal_grid.get<double>(4 * cells + (cells + 7) / 8 + 1);
-        auto* dpres = reinterpret_cast<unsigned char*>(dvh + 4 * cells);
-        auto* dradius = ctx->tmp_a.get<unsigned long long>(1);
-        CK(cudaMemcpyAsync(dvh, vg.c.data(), sizeof(double) * 4 * cells, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(dpres, vg.present.data(), cells, cudaMemcpyHostToDevice, s));
-        CK(launch_galerkin_assemble(dvh, dpres, vg.K, dk1, dk2, nb, p.kappa, v.is_constant ? 1 : 0, v.c1, v.c2, dA,
-                                    dradius, s));
-        count_launches(ctx, 2);
-        unsigned long long rbits = 0;
-        CK(cudaMemcpyAsync(&rbits, dradius, sizeof(rbits), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        double radius;
-        std::memcpy(&radius, &rbits, sizeof(radius));
-        if (radius * dt_ref >= 2.0) {
-            std::ostringstream msg;
-            msg << "galerkin_solve_ad: dt_ref " << dt_ref << " violates the stability estimate; suggest dt_ref <= "
-                << 1.8 / radius;
-            raise(SMC_ERUNTIME, msg.str());
-        }
-        // projection of theta_0 (galerkin.cpp:43-101)
-        std::vector<double> theta0;
-        if (galerkin_project_exact(p.initial_condition, m, theta0)) {
-            CK(cudaMemcpyAsync(th[0], theta0.data(), sizeof(double) * 2 * nb, cudaMemcpyHostToDevice, s));
-        } else {
-            Image im;
-            const ScalarRef ref = add_scalar(im, p.initial_condition);
-            unsigned char* base = ctx->upload(im);
-            const int n = std::max(128, 4 * (m.max_abs + 1));
-            CK(launch_galerkin_quadrature(patch(ref, base), dk1, dk2, nb, n, th[0], s));
-            count_launches(ctx, 1);
-        }
-        // the step schedule: once through the sorted observation times, shortening
-        // the last step of each segment to land on t_j (galerkin.cpp:181-221)
-        std::vector<int64_t> order(static_cast<size_t>(p.n_obs));
-        for (int64_t i = 0; i < p.n_obs; ++i) order[static_cast<size_t>(i)] = i;
-        std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return p.obs_t[a] < p.obs_t[b]; });
-        constexpr int kGroup = 16;  // even: a group returns to the buffer it started from
-        cudaGraphExec_t group[2] = {nullptr, nullptr};
-        struct GraphFree {
-            cudaGraphExec_t* g;
-            ~GraphFree() {
-                for (int i = 0; i < 2; ++i)
-                    if (g[i]) cudaGraphExecDestroy(g[i]);
-            }
-        } graph_free{group};
-        auto group_exec = [&](int cur) {
-            if (!group[cur]) {
-                cudaGraph_t graph = nullptr;
-                CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-                cudaError_t e = cudaSuccess;
-                for (int k = 0; k < kGroup && e == cudaSuccess; ++k)
-                    e = launch_galerkin_step(dA, th[(cur + k) & 1], th[(cur + k + 1) & 1], nb, dt_ref, s);
-                const cudaError_t e2 = cudaStreamEndCapture(s, &graph);
-                CK(e);
-                CK(e2);
-                const cudaError_t e3 = cudaGraphInstantiate(&group[cur], graph, 0);
-                cudaGraphDestroy(graph);
-                CK(e3);
-            }
-            return group[cur];
-        };
-        int cur = 0;
-        double t = 0.0;
-        int64_t steps = 0;
-        const bool use_graph = s != nullptr;
-        for (const int64_t oi : order) {
-            const double target = p.obs_t[oi];
-            int64_t run = 0;  // pending full steps of dt_ref
-            auto flush = [&] {
-                for (; use_graph && run >= kGroup; run -= kGroup) {
-                    CK(cudaGraphLaunch(group_exec(cur), s));
-                    count_launches(ctx, kGroup);
-                }
-                for (; run > 0; --run, cur ^= 1) {
-                    CK(launch_galerkin_step(dA, th[cur], th[cur ^ 1], nb, dt_ref, s));
-                    count_launches(ctx, 1);
-                }
-            };
-            while (t < target - 1e-15) {
-                const double dt = std::min(dt_ref, target - t);
-                if (dt == dt_ref) {
-                    ++run;
-                } else {
-                    flush();
-                    CK(launch_galerkin_step(dA, th[cur], th[cur ^ 1], nb, dt, s));
-                    count_launches(ctx, 1);
-                    cur ^= 1;
-                }
-                t += dt;
-                ++steps;
-            }
-            flush();
-            CK(launch_galerkin_observe(th[cur], dk1, dk2, nb, p.obs_x[2 * oi], p.obs_x[2 * oi + 1], dobs + oi, s));
-            count_launches(ctx, 1);
-            if (out->coefficients_at_observations)
-                CK(cudaMemcpyAsync(out->coefficients_at_observations + oi * 2 * nb, th[cur], sizeof(double) * 2 * nb,
-                                   cudaMemcpyDeviceToHost, s));
-        }
-        CK(cudaMemcpyAsync(out->observation_values, dobs, sizeof(double) * p.n_obs, cudaMemcpyDeviceToHost, s));
-        if (out->final_coefficients)
-            CK(cudaMemcpyAsync(out->final_coefficients, th[cur], sizeof(double) * 2 * nb, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        out->dt_used = dt_ref;
-        out->steps = steps;
-    });
-}
-
-smc_status smc_galerkin_field_grid(smc_ctx* ctx, const smc_galerkin_basis* basis, const double* coefficients,
-                                   int32_t n, double* grid) {
-    return guarded([&] {
-        CK(cudaSetDevice(ctx->device));
-        if (n < 2) raise(SMC_EINVAL, "galerkin_field_grid: n must be >= 2");
-        const GalerkinModes m = galerkin_modes(*basis);
-        const int64_t nb = m.size();
-        cudaStream_t s = ctx->stream;
-        double* dc = ctx->gal_t0.get<double>(static_cast<size_t>(2 * nb));
-        int* dk1 = ctx->gal_k1.get<int>(static_cast<size_t>(nb));
-        int* dk2 = ctx->gal_k2.get<int>(static_cast<size_t>(nb));
-        double* dg = ctx->gal_grid.get<double>(static_cast<size_t>(n) * n);
-        CK(cudaMemcpyAsync(dc, coefficients, sizeof(double) * 2 * nb, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(dk1, m.k1.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(dk2, m.k2.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, s));
-        CK(launch_galerkin_field_grid(dc, dk1, dk2, nb, n, dg, s));
-        count_launches(ctx, 1);
-        CK(cudaMemcpyAsync(grid, dg, sizeof(double) * n * n, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-    });
-}
-
 smc_status smc_fp64_peak(smc_ctx* ctx, double ms, double* tflops) {
     return guarded([&] {
         CK(cudaSetDevice(ctx->device));
@@ -1006,263 +592,6 @@ smc_status smc_fp64_peak(smc_ctx* ctx, double ms, double* tflops) {
         }
         const double flops = 2.0 * 8.0 * double(iters) * 256.0 * blocks;
         *tflops = flops / (double(t) * 1e-3) / 1e12;
-    });
-}
-
-int64_t smc_pcn_num_samples(const smc_chain_config* cfg) {
-    // iterations i = 1..n_steps with i > burn_in and (i - burn_in - 1) % thin == 0
-    if (!cfg || cfg->thin < 1 || cfg->n_steps <= cfg->burn_in) return 0;
-    const int64_t burn = cfg->burn_in < 0 ? 0 : cfg->burn_in;
-    return (cfg->n_steps - burn - 1) / cfg->thin + 1;
-}
-
-smc_status smc_pcn_chains(smc_ctx* ctx, const smc_ad_problem* forward, const smc_prior* prior, const double* data,
-                          double noise_std, uint64_t forward_seed, int64_t n_chains, const uint64_t* chain_seeds,
-                          const double* u0, const smc_chain_config* cfg, smc_chain_outputs* out) {
-    return guarded([&] {
-        CK(cudaSetDevice(ctx->device));
-        // run_chain's checks (inference.cpp:172-173), prior_draw/chain_init's
-        // (inference.cpp:17-21, :89-91, :125-133), pcn_step's (:138).
-        if (cfg->n_steps < 0) raise(SMC_EINVAL, "run_chain: n_steps must be >= 0");
-        if (cfg->thin < 1) raise(SMC_EINVAL, "run_chain: thin must be >= 1");
-        if (prior->cutoff < 1) raise(SMC_EINVAL, "PriorSpec: cutoff must be >= 1");
-        if (!(prior->s0 >= 0.0)) raise(SMC_EINVAL, "PriorSpec: s0 must be >= 0");
-        if (!std::isfinite(prior->alpha)) raise(SMC_EINVAL, "PriorSpec: alpha must be finite");
-        if (!(noise_std > 0.0)) raise(SMC_EINVAL, "LikelihoodSpec: noise_std must be positive");
-        if (cfg->n_steps > 0 && !(cfg->beta > 0.0 && cfg->beta <= 1.0))
-            raise(SMC_EINVAL, "pcn_step: beta must be in (0,1]");
-        if (n_chains < 1) raise(SMC_EINVAL, "pcn_chains: need at least one chain");
-        if (!out || !out->final_u) raise(SMC_EINVAL, "pcn_chains: final_u output is required");
-        smc_ad_problem p = *forward;
-        check_kappa(p.kappa);
-        check_scalar(p.initial_condition);
-        ad_validate(p);
-        check_particle_range(p.n_particles);
-        if (p.precision == SMC_FP64_STRICT) raise(SMC_EINVAL, "strict precision is single-sample only");
-        cudaStream_t s = ctx->stream;
-        const int64_t n_obs = p.n_obs, n = p.n_particles, B = n_chains;
-
-        // prior modes (|k|^2 then (k1,k2) order) and per-mode stds (inference.cpp:24-53)
-        const std::vector<HostMode> pm = prior_modes(prior->cutoff);
-        const int64_t M = static_cast<int64_t>(pm.size()), dim = 2 * M;
-        std::vector<double> stds(static_cast<size_t>(M));
-        for (int64_t i = 0; i < M; ++i) {
-            const double kn = std::sqrt(double(pm[i].k1) * pm[i].k1 + double(pm[i].k2) * pm[i].k2);
-            stds[static_cast<size_t>(i)] = prior->s0 * std::pow(kn, -prior->alpha);
-        }
-        // lattice structure of the full prior disk and the u -> block gather map
-        // (disk layout for K <= kDiskMaxK, tiled lattice otherwise)
-        const PreparedVelocity structure = prior_structure(prior->cutoff);
-        const bool use_disk = prior->cutoff <= kDiskMaxK && std::getenv("SMC_DISABLE_DISK") == nullptr;
-        const LatticeHost Lh = lattice_structure(structure);
-        const PackMap pmap = pack_map(prior->cutoff, use_disk, &Lh);
-        const int64_t stride = pmap.stride;
-        if (static_cast<int64_t>(p.n_obs) <= 0) raise(SMC_EINVAL, "AdProblemSpec: no observations");
-
-        // device buffers (freed at the end of the call)
-        std::vector<void*> owned;
-        auto dalloc = [&](size_t bytes) {
-            void* q = nullptr;
-            CK(cudaMalloc(&q, std::max<size_t>(bytes, 16)));
-            owned.push_back(q);
-            return q;
-        };
-        struct Freer {
-            std::vector<void*>* v;
-            ~Freer() {
-                for (void* q : *v) cudaFree(q);
-            }
-        } freer{&owned};
-        auto h2d = [&](void* dst, const void* src, size_t bytes) {
-            CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
-        };
-        const int64_t n_samples = smc_pcn_num_samples(cfg);
-        PcnStep S{};
-        S.n_chains = B;
-        S.dim = dim;
-        S.M = M;
-        S.n_obs = n_obs;
-        S.n_steps = cfg->n_steps;
-        S.n_samples = n_samples;
-        S.noise_std = noise_std;
-        S.noise_inf = std::isinf(noise_std) ? 1 : 0;
-        auto* d_stds = static_cast<double*>(dalloc(8 * M));
-        h2d(d_stds, stds.data(), 8 * M);
-        S.stds = d_stds;
-        auto* d_seeds = static_cast<uint64_t*>(dalloc(8 * B));
-        h2d(d_seeds, chain_seeds, 8 * B);
-        S.seeds = d_seeds;
-        auto* d_data = static_cast<double*>(dalloc(8 * n_obs));
-        h2d(d_data, data, 8 * n_obs);
-        S.data = d_data;
-        const PackDev pdev = upload_pack_map(ctx, pmap);
-        S.U = static_cast<double*>(dalloc(8 * B * dim));
-        S.Up = static_cast<double*>(dalloc(8 * B * dim));
-        S.map_u = static_cast<double*>(dalloc(8 * B * dim));
-        S.norm_prop = static_cast<double*>(dalloc(8 * B));
-        S.norm_cur = static_cast<double*>(dalloc(8 * B));
-        S.phi = static_cast<double*>(dalloc(8 * B));
-        S.map_obj = static_cast<double*>(dalloc(8 * B));
-        S.accepted = static_cast<int64_t*>(dalloc(8 * B));
-        S.acc_flag = static_cast<uint8_t*>(dalloc(B));
-        S.map_flag = static_cast<uint8_t*>(dalloc(B));
-        S.phi_trace = out->phi_trace ? static_cast<double*>(dalloc(8 * B * std::max<int64_t>(1, cfg->n_steps))) : nullptr;
-        S.samples = (out->samples && n_samples > 0) ? static_cast<double*>(dalloc(8 * B * n_samples * dim)) : nullptr;
-        auto* d_blocks = static_cast<double*>(dalloc(8 * B * stride));
-        CK(cudaMemsetAsync(S.U, 0, 8 * B * dim, s));
-        CK(cudaMemsetAsync(S.accepted, 0, 8 * B, s));
-        CK(cudaMemsetAsync(S.phi, 0, 8 * B, s));
-
-        // forward image (theta_0, observations, lattice tiles); coefficient
-        // blocks come from the pack kernel
-        p.velocity.is_constant = 0;
-        p.velocity.max_wavenumber = prior->cutoff;
-        AdPrepared P = prepare_ad(ctx, p, {&structure}, structure, 0, n_obs);
-        P.L.seed = forward_seed;
-        P.L.seeds = nullptr;
-        if (!use_disk) {
-            P.L.vel.lat.coef = d_blocks;
-            P.L.vel.lat.sample_stride = stride;
-        }
-        double* values = ctx->values.get<double>(static_cast<size_t>(B * n_obs * n));
-
-        auto forward_map = [&]() -> smc_estimate* {
-            for (int64_t b0 = 0; b0 < B; b0 += 65535)
-                CK(launch_pack(pdev, S.Up + b0 * dim, dim, std::min<int64_t>(65535, B - b0), d_blocks + b0 * stride,
-                               nullptr, s));
-            constexpr int64_t kMaxZ = 65535;
-            for (int64_t b0 = 0; b0 < B; b0 += kMaxZ) {
-                AdLaunch L = P.L;
-                L.n_samples = static_cast<int32_t>(std::min(kMaxZ, B - b0));
-                L.values = values + b0 * n_obs * n;
-                if (use_disk) {
-                    CK(launch_ad_disk(L, prior->cutoff, d_blocks + b0 * stride, s));
-                } else {
-                    L.vel.lat.coef = d_blocks + b0 * stride;
-                    run_particles(ctx, L);
-                }
-            }
-            count_launches(ctx, 1);
-            return reduce_ad_device(ctx, values, n, B * n_obs);
-        };
-
-        // chain_init (inference.cpp:125-134): u0 given, or prior_draw from the stream
-        uint64_t blk = 0;
-        if (u0) {
-            h2d(S.U, u0, 8 * B * dim);
-            S.contraction = 1.0;  // Up = 1 U + 0 xi = U
-            S.beta = 0.0;
-        } else {
-            S.contraction = 0.0;  // Up = 0 U + 1 xi = xi = prior_draw
-            S.beta = 1.0;
-            blk = static_cast<uint64_t>(M);
-        }
-        S.blk0 = 0;
-        S.init = 1;
-        S.step = 0;
-        S.sample_slot = -1;
-        CK(launch_pcn_propose(S, s));
-        CK(launch_pcn_accept(S, forward_map(), s));
-        CK(launch_pcn_commit(S, s));
-        count_launches(ctx, 3);
-
-        // the steps (pcn_step, inference.cpp:136-166; run_chain loop :182-189)
-        S.init = 0;
-        S.contraction = std::sqrt(1.0 - cfg->beta * cfg->beta);
-        S.beta = cfg->beta;
-        ctx->stats = smc_stats{};
-        CK(cudaEventRecord(ctx->ev[0], s));
-        const char* ge = std::getenv("SMC_PCN_GRAPH");
-        const bool use_graph = cfg->n_steps >= 2 && s != nullptr && !(ge && std::atoi(ge) == 0);
-        if (use_graph) {
-            // Graph mode: the step index is a device counter, so a captured
-            // group of G steps (propose, pack, K1, K3, accept, commit, advance)
-            // replays unchanged; the launch cost per step drops to a share of
-            // one graph launch.  Same kernels, same arguments: bit-identical.
-            auto* d_it = static_cast<int64_t*>(dalloc(8));
-            CK(cudaMemsetAsync(d_it, 0, 8, s));
-            S.it_dev = d_it;
-            S.blk_base = blk;
-            S.burn_in = cfg->burn_in;
-            S.thin = cfg->thin;
-            const int64_t before = ctx->total_launches;
-            auto capture = [&](int64_t g) {
-                cudaGraph_t graph = nullptr;
-                CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-                try {
-                    for (int64_t k = 0; k < g; ++k) {
-                        CK(launch_pcn_propose(S, s));
-                        CK(launch_pcn_accept(S, forward_map(), s));
-                        CK(launch_pcn_commit(S, s));
-                        CK(launch_pcn_advance(d_it, s));
-                    }
-                } catch (...) {
-                    cudaStreamEndCapture(s, &graph);
-                    if (graph) cudaGraphDestroy(graph);
-                    throw;
-                }
-                CK(cudaStreamEndCapture(s, &graph));
-                cudaGraphExec_t exec = nullptr;
-                const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
-                cudaGraphDestroy(graph);
-                CK(e);
-                return exec;
-            };
-            const int64_t G = std::min<int64_t>(16, cfg->n_steps);
-            cudaGraphExec_t group = capture(G);
-            const int64_t per_step = (ctx->total_launches - before) / G + 4;
-            const int64_t rest = cfg->n_steps % G;
-            cudaGraphExec_t single = rest ? capture(1) : nullptr;
-            struct ExecFree {
-                cudaGraphExec_t a, b;
-                ~ExecFree() {
-                    if (a) cudaGraphExecDestroy(a);
-                    if (b) cudaGraphExecDestroy(b);
-                }
-            } exec_free{group, single};
-            for (int64_t q = 0; q < cfg->n_steps / G; ++q) CK(cudaGraphLaunch(group, s));
-            for (int64_t r = 0; r < rest; ++r) CK(cudaGraphLaunch(single, s));
-            ctx->total_launches = before + per_step * cfg->n_steps;
-        }
-        bool ucache = false;
-        uint64_t ublk = 0;
-        for (int64_t it = 0; !use_graph && it < cfg->n_steps; ++it) {
-            S.blk0 = blk;
-            blk += static_cast<uint64_t>(M);
-            if (!ucache) {  // uniform() draws a fresh block and caches its second value
-                ublk = blk;
-                blk += 1;
-                S.uhalf = 0;
-                ucache = true;
-            } else {
-                S.uhalf = 1;
-                ucache = false;
-            }
-            S.ublk = ublk;
-            S.step = it;
-            const int64_t iteration = it + 1;
-            S.sample_slot = (iteration > cfg->burn_in && (iteration - cfg->burn_in - 1) % cfg->thin == 0)
-                                ? (iteration - std::max<int64_t>(cfg->burn_in, 0) - 1) / cfg->thin
-                                : -1;
-            CK(launch_pcn_propose(S, s));
-            CK(launch_pcn_accept(S, forward_map(), s));
-            CK(launch_pcn_commit(S, s));
-            count_launches(ctx, 3);
-        }
-        CK(cudaEventRecord(ctx->ev[1], s));
-        CK(cudaEventRecord(ctx->ev[2], s));
-        auto d2h = [&](void* dst, const void* src, size_t bytes) {
-            if (dst) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
-        };
-        d2h(out->final_u, S.U, 8 * B * dim);
-        d2h(out->final_phi, S.phi, 8 * B);
-        d2h(out->map_u, S.map_u, 8 * B * dim);
-        d2h(out->map_objective, S.map_obj, 8 * B);
-        d2h(out->accepted, S.accepted, 8 * B);
-        if (S.phi_trace && cfg->n_steps > 0) d2h(out->phi_trace, S.phi_trace, 8 * B * cfg->n_steps);
-        if (S.samples) d2h(out->samples, S.samples, 8 * B * n_samples * dim);
-        CK(cudaStreamSynchronize(s));
-        finish_stats(ctx);  // particle_kernel_ms = device time of the step loop
     });
 }
 

@@ -1,0 +1,195 @@
+// capi_internal.h — shared internals of the C ABI translation units
+// (capi.cu: context, images, AD/BVP forward maps; capi_samples.cu: batched
+// evaluations and multi-chain pCN; capi_galerkin.cu: the spectral reference
+// solver).  Not part of the public interface.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <sstream>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/scalarmc_b200.h"
+#include "disk_shape.h"
+#include "host_problem.h"
+#include "kernels.h"
+
+namespace smc::capi {
+
+constexpr int kLatticeTileHost = 8;  // == kLatticeTile (velocity.cuh) / kTileW (host_problem.cpp)
+
+extern thread_local std::string g_err;
+
+
+
+#define CK(x)                                                                                       \
+    do {                                                                                            \
+        cudaError_t e_ = (x);                                                                       \
+        if (e_ != cudaSuccess) ::smc::raise(SMC_ECUDA, std::string("CUDA error: ") + cudaGetErrorString(e_) + \
+                                                    " (" #x ")");                                   \
+    } while (0)
+
+template <class F>
+smc_status guarded(F&& f) {
+    try {
+        f();
+        return SMC_OK;
+    } catch (const Error& e) {
+        g_err = e.msg;
+        return static_cast<smc_status>(e.code);
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return SMC_ERUNTIME;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return SMC_ERUNTIME;
+    }
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    template <class T>
+    T* get(size_t n) {
+        const size_t bytes = std::max<size_t>(n * sizeof(T), 16);
+        if (bytes > cap) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            cap = 0;
+            CK(cudaMalloc(&p, bytes));
+            cap = bytes;
+        }
+        return static_cast<T*>(p);
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+struct PinnedBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    template <class T>
+    T* get(size_t n) {
+        const size_t bytes = std::max<size_t>(n * sizeof(T), 16);
+        if (bytes > cap) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            cap = 0;
+            CK(cudaMallocHost(&p, bytes));
+            cap = bytes;
+        }
+        return static_cast<T*>(p);
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+// Host-side image under construction: 16-byte aligned blobs in one arena.
+struct Image {
+    std::vector<unsigned char> bytes;
+    size_t add(const void* src, size_t n) {
+        const size_t off = (bytes.size() + 15) & ~size_t(15);
+        bytes.resize(off + std::max<size_t>(n, 1));
+        if (n) std::memcpy(bytes.data() + off, src, n);
+        return off;
+    }
+    template <class T>
+    size_t add_vec(const std::vector<T>& v) {
+        return add(v.data(), v.size() * sizeof(T));
+    }
+    size_t reserve(size_t n) {
+        const size_t off = (bytes.size() + 15) & ~size_t(15);
+        bytes.resize(off + std::max<size_t>(n, 1));
+        return off;
+    }
+};
+
+
+}  // namespace smc::capi
+
+using smc::capi::DevBuf;
+using smc::capi::Image;
+using smc::capi::PinnedBuf;
+
+struct smc_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;      // stream every launch goes to
+    cudaStream_t own_stream = nullptr;  // the context's own stream
+    int64_t total_launches = 0;
+    cudaEvent_t ev[4] = {};
+    DevBuf image, values, aux, flags, flags2, scratch, sums, means, sumsq, sumaux, est, counts, tmp_a, tmp_b, tmp_c;
+    DevBuf pk_ip, pk_im, pk_kp, pk_km, pk_ms, pk_u, pk_blocks, pk_bad;  // device u -> field packing
+    DevBuf gal_A, gal_t0, gal_t1, gal_k1, gal_k2, gal_obs, gal_grid;  // Galerkin reference solver
+    PinnedBuf staging, est_host;
+    smc_stats stats{};
+    // sharded AD state (smc_ad_shard_*)
+    int64_t shard_n_obs = 0, shard_span = 0;
+
+    unsigned char* upload(const Image& img) {
+        unsigned char* h = staging.get<unsigned char>(img.bytes.size());
+        std::memcpy(h, img.bytes.data(), img.bytes.size());
+        unsigned char* d = image.get<unsigned char>(img.bytes.size());
+        CK(cudaMemcpyAsync(d, h, img.bytes.size(), cudaMemcpyHostToDevice, stream));
+        return d;
+    }
+};
+
+namespace smc::capi {
+
+void count_launches(smc_ctx* ctx, int64_t n);
+
+// ScalarField image: term arrays appended to the image; pointers patched
+// after upload.
+struct ScalarRef {
+    ScalarImg img{};
+    size_t amp = 0, freq = 0, phase = 0, center = 0;
+};
+ScalarRef add_scalar(Image& im, const smc_scalar_field& f);
+ScalarImg patch(const ScalarRef& r, unsigned char* base);
+
+struct VelRef {
+    VelImg img{};
+    size_t modes = 0, tiles = 0, coefs = 0;
+};
+// Velocity image: strict mode list + tiled lattice structure + one
+// coefficient block per sample (fills[i] for sample i).
+VelRef add_velocity(Image& im, const PreparedVelocity& v, const std::vector<const PreparedVelocity*>& fills);
+VelImg patch(const VelRef& r, unsigned char* base);
+
+// Everything a K1 launch needs, prepared and uploaded.
+struct AdPrepared {
+    AdLaunch L{};
+    int disk_K = 0;                  // > 0: use the compile-time disk kernel
+    const double* disk = nullptr;    // its coefficient blocks (device, one per sample)
+    int64_t n_obs = 0;
+    int64_t steps_per_particle_sum = 0;  // sum_j n_j
+};
+void check_particle_range(int64_t n_particles);
+AdPrepared prepare_ad(smc_ctx* ctx, const smc_ad_problem& p, const std::vector<const PreparedVelocity*>& fills,
+                      const PreparedVelocity& structure, int64_t obs_begin, int64_t obs_count);
+void run_particles(smc_ctx* ctx, AdLaunch& L, const AdPrepared* P = nullptr, int64_t sample0 = 0);
+// Reduce [n_seg][n] values (no failures) into estimates left on the device.
+smc_estimate* reduce_ad_device(smc_ctx* ctx, const double* values, int64_t n, int64_t n_seg);
+// ... and copied to the host.
+void reduce_ad(smc_ctx* ctx, const double* values, int64_t n, int64_t n_seg, smc_estimate* out);
+void finish_stats(smc_ctx* ctx);
+void ad_observe_range(smc_ctx* ctx, const smc_ad_problem& p, uint64_t seed, int64_t obs_begin, int64_t obs_count,
+                      smc_estimate* out);
+BvpLaunch prepare_bvp(smc_ctx* ctx, const smc_bvp_problem& p, int64_t obs_begin, int64_t obs_count);
+void run_bvp(smc_ctx* ctx, BvpLaunch& L, int64_t n_obs, int64_t n);
+// Upload a PackMap into the context's pack buffers (reused across calls).
+PackDev upload_pack_map(smc_ctx* ctx, const PackMap& m);
+
+}  // namespace smc::capi
