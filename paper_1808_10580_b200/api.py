@@ -609,399 +609,11 @@ def philox_device(ctr: np.ndarray, key: np.ndarray, ctx: Context | None = None) 
     return out
 
 
-# ---------------------------------------------------------------------------
-# u -> G callers (inference.hpp, optimize.hpp)
-# ---------------------------------------------------------------------------
-@dataclass(frozen=True)
-class PriorSpec:
-    """PriorSpec (inference.hpp:22-38)."""
-    cutoff: int = 8
-    s0: float = 1.0
-    alpha: float = 2.5
-
-    def validate(self) -> None:
-        if self.cutoff < 1:
-            raise ValueError("PriorSpec: cutoff must be >= 1")
-        if not self.s0 >= 0.0:
-            raise ValueError("PriorSpec: s0 must be >= 0")
-        if not math.isfinite(self.alpha):
-            raise ValueError("PriorSpec: alpha must be finite")
-
-    def modes(self) -> list[tuple[int, int]]:
-        """Canonical modes ordered by |k|^2 then (k1, k2) (inference.cpp:24-40)."""
-        K = self.cutoff
-        out = [(k1, k2) for k1 in range(-K, K + 1) for k2 in range(-K, K + 1)
-               if (k1 > 0 or (k1 == 0 and k2 > 0)) and float(k1) * k1 + float(k2) * k2 <= float(K) * K]
-        out.sort(key=lambda m: (float(m[0]) * m[0] + float(m[1]) * m[1], m[0], m[1]))
-        return out
-
-    def component_stds(self) -> np.ndarray:
-        s = [self.s0 * math.pow(math.sqrt(float(a) * a + float(b) * b), -self.alpha) for a, b in self.modes()]
-        return np.repeat(np.asarray(s, dtype=np.float64), 2)
-
-    def dimension(self) -> int:
-        return 2 * len(self.modes())
-
-    def _pod(self) -> A.smc_prior:
-        p = A.smc_prior()
-        p.cutoff, p.s0, p.alpha = self.cutoff, self.s0, self.alpha
-        return p
-
-
-def prior_draw(prior: PriorSpec, seed: int, obs_index: int, particle_index: int, ctx: Context | None = None) -> np.ndarray:
-    """prior_draw (inference.cpp:55-61) for a fresh NormalStream{seed, obs,
-    particle}: u_i = s_i * normal(), normals drawn pairwise (rng.cpp:74-83) on
-    the device."""
-    prior.validate()
-    stds = prior.component_stds()
-    z = normal_pairs_device(seed, obs_index, particle_index, len(stds) // 2 + 1, ctx).reshape(-1)
-    return stds * z[: len(stds)]
-
-
-def velocity_from_coefficients(prior: PriorSpec, u: Sequence[float]) -> FourierVelocityField:
-    """inference.cpp:63-73."""
-    modes = prior.modes()
-    u = np.asarray(u, dtype=np.float64)
-    if u.shape != (2 * len(modes),):
-        raise ValueError("velocity_from_coefficients: coefficient size mismatch")
-    return FourierVelocityField.from_arrays(np.asarray(modes, dtype=np.int32), u.reshape(-1, 2), prior.cutoff)
-
-
-@dataclass
-class LikelihoodSpec:
-    """LikelihoodSpec (inference.hpp:52-59)."""
-    data: list
-    noise_std: float = 0.1
-    forward: AdProblemSpec = field(default_factory=AdProblemSpec)
-    forward_seed: int = 0
-    workers: int = 1
-
-    def validate(self) -> None:
-        if len(self.data) != len(self.forward.observations):
-            raise ValueError("LikelihoodSpec: data length must match observation count")
-        if not self.noise_std > 0.0:
-            raise ValueError("LikelihoodSpec: noise_std must be positive")
-
-    def misfit(self, prior: PriorSpec, u: Sequence[float]) -> float:
-        """Phi(u) = |y - G(u)|^2 / (2 sigma_n^2) (inference.cpp:93-104)."""
-        if math.isinf(self.noise_std):
-            return 0.0
-        spec = replace(self.forward, velocity=VelocityField.fourier(velocity_from_coefficients(prior, u)))
-        est = observe_ad(spec, self.forward_seed, self.workers)
-        ss = 0.0
-        for y, e in zip(self.data, est):
-            r = y - e.mean
-            ss += r * r
-        return ss / (2.0 * self.noise_std * self.noise_std)
-
-    def misfit_batched(self, prior: PriorSpec, U: np.ndarray) -> np.ndarray:
-        """Phi for every row of U in one batched launch (common random numbers,
-        the same forward_seed for every row, as misfit)."""
-        est = observe_ad_batched(self.forward, prior, U, self.forward_seed)
-        r = np.asarray(self.data, dtype=np.float64)[None, :] - est["mean"]
-        return (r * r).sum(axis=1) / (2.0 * self.noise_std * self.noise_std)
-
-
-@dataclass
-class ChainConfig:
-    """ChainConfig (inference.hpp:87-93)."""
-    n_steps: int = 10000
-    beta: float = 0.02
-    burn_in: int = 0
-    thin: int = 1
-    seed: int = 0
-
-
-def run_chains(config: ChainConfig, prior: PriorSpec, likelihood: LikelihoodSpec, seeds: Sequence[int],
-               u0: np.ndarray | None = None, keep_samples: bool = True, keep_trace: bool = True,
-               ctx: Context | None = None) -> dict:
-    """len(seeds) independent pCN chains on the device (run_chain,
-    inference.cpp:170-194): chain c is run_chain(config with seed=seeds[c]),
-    and every step evaluates all chains' proposals in one batched forward
-    map.  Returns arrays: final_u [B][dim], final_phi [B], map_u [B][dim],
-    map_objective [B], accepted [B], acceptance_rate [B], phi_trace
-    [B][n_steps], samples [B][n_samples][dim]."""
-    ctx = ctx or default_context()
-    likelihood.validate()
-    p, keep = likelihood.forward._pod()
-    seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
-    B, dim = len(seeds), prior.dimension()
-    cfg = A.smc_chain_config(config.n_steps, config.beta, config.burn_in, config.thin)
-    ns = int(ctx.lib.smc_pcn_num_samples(C.byref(cfg)))
-    res = {"final_u": np.zeros((B, dim)), "final_phi": np.zeros(B), "map_u": np.zeros((B, dim)),
-           "map_objective": np.zeros(B), "accepted": np.zeros(B, dtype=np.int64)}
-    res["phi_trace"] = np.zeros((B, max(config.n_steps, 1))) if keep_trace else None
-    res["samples"] = np.zeros((B, max(ns, 1), dim)) if keep_samples and ns > 0 else None
-    out = A.smc_chain_outputs(A.dptr(res["final_u"]), A.dptr(res["final_phi"]), A.dptr(res["map_u"]),
-                              A.dptr(res["map_objective"]), res["accepted"].ctypes.data_as(C.POINTER(C.c_int64)),
-                              A.dptr(res["phi_trace"]), A.dptr(res["samples"]))
-    d = np.ascontiguousarray(likelihood.data, dtype=np.float64)
-    u0p = A.dptr(np.ascontiguousarray(u0, dtype=np.float64).reshape(B, dim)) if u0 is not None else A.dptr(None)
-    _check(ctx.lib.smc_pcn_chains(ctx.handle, C.byref(p), C.byref(prior._pod()), A.dptr(d),
-                                  C.c_double(likelihood.noise_std), C.c_uint64(likelihood.forward_seed), B,
-                                  seeds.ctypes.data_as(C.POINTER(C.c_uint64)), u0p, C.byref(cfg), C.byref(out)))
-    if keep_trace:
-        res["phi_trace"] = res["phi_trace"][:, : config.n_steps]
-    if res["samples"] is not None:
-        res["samples"] = res["samples"][:, :ns]
-    res["acceptance_rate"] = res["accepted"] / max(config.n_steps, 1) if config.n_steps > 0 else np.zeros(B)
-    return res
-
-
-@dataclass
-class ForcingControl:
-    """ForcingControl (optimize.hpp:45-54)."""
-    initial_amplitudes: list
-    centers: list
-    sharpness: float = 4.0
-    target: list = field(default_factory=list)
-    observation_points: list = field(default_factory=list)
-
-    def validate(self) -> None:
-        if not self.centers:
-            raise ValueError("ForcingControl: no forcing centers")
-        if len(self.initial_amplitudes) != len(self.centers):
-            raise ValueError("ForcingControl: amplitude/center count mismatch")
-        if len(self.target) != len(self.observation_points):
-            raise ValueError("ForcingControl: target and observation lengths must match")
-        if not self.sharpness > 0.0:
-            raise ValueError("ForcingControl: sharpness must be positive")
-
-
-def _control_spec(control: ForcingControl, base: BvpProblemSpec, amplitudes: Sequence[float]) -> BvpProblemSpec:
-    """control_spec (optimize.cpp:147-157)."""
-    return replace(base, forcing=ScalarField.gaussian_bumps(
-        [Bump(float(a), Vec2(*c)) for a, c in zip(amplitudes, control.centers)], control.sharpness),
-        observations=list(control.observation_points))
-
-
-@dataclass(frozen=True)
-class ForcingBasis:
-    """One Dirichlet pass under common random numbers, linear in the bump
-    amplitudes F: mean_j(F) = bc[j] - basis[j] . F (smc_bvp_forcing_basis)."""
-    bc: np.ndarray        # [n_obs] E[theta_bc(X_tau)]
-    basis: np.ndarray     # [n_obs][n_bumps] E[int phi_k(X_t) dt]
-    exit_time: np.ndarray # [n_obs]
-    n_failed: np.ndarray  # [n_obs]
-
-    def means(self, amplitudes: Sequence[float]) -> np.ndarray:
-        return self.bc - self.basis @ np.asarray(amplitudes, dtype=np.float64)
-
-
-def forcing_basis(control: ForcingControl, base: BvpProblemSpec, seed: int, ctx: Context | None = None) -> ForcingBasis:
-    ctx = ctx or default_context()
-    control.validate()
-    spec = _control_spec(control, base, [1.0] * len(control.centers))
-    p, keep = spec._pod()
-    nb, no = len(control.centers), len(control.observation_points)
-    bc, tau = np.zeros(no), np.zeros(no)
-    basis = np.zeros((no, nb))
-    nf = np.zeros(no, dtype=np.int64)
-    _check(ctx.lib.smc_bvp_forcing_basis(ctx.handle, C.byref(p), C.c_uint64(seed), A.dptr(bc), A.dptr(basis),
-                                         A.dptr(tau), nf.ctypes.data_as(C.POINTER(C.c_int64))))
-    return ForcingBasis(bc, basis, tau, nf)
-
-
-@dataclass
-class NelderMeadOptions:
-    """NelderMeadOptions (optimize.hpp:13-21)."""
-    x_tol: float = 1e-6
-    f_tol: float = 1e-9
-    max_iter: int = 2000
-    initial_step: float = 1.0
-
-
-def nelder_mead(objective, x0: Sequence[float], options: NelderMeadOptions = NelderMeadOptions()) -> dict:
-    """nelder_mead (optimize.cpp:37-134): coefficients (1, 2, 0.5, 0.5),
-    non-finite values as +inf, stops on simplex diameter < x_tol, value spread
-    < f_tol, or max_iter (the reference's algorithm, restated on the host)."""
-    dim = len(x0)
-    if dim == 0:
-        raise ValueError("nelder_mead: empty start point")
-    if not all(math.isfinite(v) for v in x0):
-        raise ValueError("nelder_mead: non-finite start point")
-
-    def guarded(x):
-        v = objective(x)
-        return v if math.isfinite(v) else math.inf
-
-    verts = [list(map(float, x0)) for _ in range(dim + 1)]
-    for i in range(dim):
-        verts[i + 1][i] += options.initial_step
-    vals = [guarded(v) for v in verts]
-
-    def sort_simplex():
-        nonlocal verts, vals
-        order = sorted(range(dim + 1), key=lambda i: vals[i])  # stable, like std::stable_sort
-        verts = [verts[i] for i in order]
-        vals = [vals[i] for i in order]
-
-    def diameter():
-        d = 0.0
-        for i in range(1, dim + 1):
-            s = 0.0
-            for c in range(dim):
-                diff = verts[i][c] - verts[0][c]
-                s += diff * diff
-            d = max(d, math.sqrt(s))
-        return d
-
-    sort_simplex()
-    trace = [(0, vals[0], list(verts[0]))]
-    it, reason = 0, "max_iter"
-    while it < options.max_iter:
-        if diameter() < options.x_tol:
-            reason = "x_tol"
-            break
-        if math.isfinite(vals[dim]) and vals[dim] - vals[0] < options.f_tol:
-            reason = "f_tol"
-            break
-        centroid = [0.0] * dim
-        for i in range(dim):
-            for c in range(dim):
-                centroid[c] += verts[i][c] / float(dim)
-
-        def along(t):
-            return [centroid[c] + t * (centroid[c] - verts[dim][c]) for c in range(dim)]
-
-        refl = along(1.0)
-        f_refl = guarded(refl)
-        if f_refl < vals[0]:
-            exp_ = along(2.0)
-            f_exp = guarded(exp_)
-            if f_exp < f_refl:
-                verts[dim], vals[dim] = exp_, f_exp
-            else:
-                verts[dim], vals[dim] = refl, f_refl
-        elif f_refl < vals[dim - 1]:
-            verts[dim], vals[dim] = refl, f_refl
-        else:
-            outside = f_refl < vals[dim]
-            con = along(0.5 if outside else -0.5)
-            f_con = guarded(con)
-            if f_con < min(vals[dim], f_refl):
-                verts[dim], vals[dim] = con, f_con
-            else:
-                for i in range(1, dim + 1):
-                    verts[i] = [verts[0][c] + 0.5 * (verts[i][c] - verts[0][c]) for c in range(dim)]
-                    vals[i] = guarded(verts[i])
-        sort_simplex()
-        it += 1
-        trace.append((it, vals[0], list(verts[0])))
-    return {"argmin": verts[0], "min_value": vals[0], "iterations": it, "stop_reason": reason, "trace": trace}
-
-
-def optimize_forcing(control: ForcingControl, base: BvpProblemSpec, options: NelderMeadOptions, seed: int,
-                     ctx: Context | None = None) -> dict:
-    """optimize_forcing (optimize.cpp:175-185) with every Nelder-Mead vertex
-    evaluated from ONE device pass (forcing_basis): under the fixed seed the
-    objective |Y - G(F)|_2 is exactly the reference's forcing_cost up to
-    summation order (G is linear in F)."""
-    control.validate()
-    fb = forcing_basis(control, base, seed, ctx)
-    Y = np.asarray(control.target, dtype=np.float64)
-
-    def cost(F):
-        r = Y - fb.means(F)
-        return math.sqrt(float(np.sum(r * r)))
-    res = nelder_mead(cost, control.initial_amplitudes, options)
-    res["basis"] = fb
-    return res
-
-
-def forcing_cost(amplitudes: Sequence[float], control: ForcingControl, base: BvpProblemSpec, seed: int,
-                 workers: int = 1) -> float:
-    """|Y - G(F)|_2 with G = observe_bvp under a fixed seed (optimize.cpp:161-173)."""
-    control.validate()
-    if len(amplitudes) != len(control.centers):
-        raise ValueError("forcing_cost: amplitude count mismatch")
-    est = observe_bvp(_control_spec(control, base, amplitudes), seed, workers)
-    ss = 0.0
-    for y, e in zip(control.target, est):
-        r = y - e.mean
-        ss += r * r
-    return math.sqrt(ss)
-
-
-# ---------------------------------------------------------------------------
-# spectral Galerkin reference solver (SURVEY.md §8(f) rank 4)
-# ---------------------------------------------------------------------------
-@dataclass(frozen=True)
-class GalerkinBasis:
-    """GalerkinBasis (galerkin.hpp:14-18): `box` keeps max(|l1|,|l2|) <= cutoff,
-    `disk` keeps |l|_2 <= cutoff."""
-    kind: str = "box"
-    cutoff: int = 8
-
-    def _pod(self) -> A.smc_galerkin_basis:
-        if self.kind not in ("box", "disk"):
-            raise ValueError("GalerkinBasis: kind must be 'box' or 'disk'")
-        return A.smc_galerkin_basis(0 if self.kind == "box" else 1, int(self.cutoff))
-
-    def modes(self) -> list[tuple[int, int]]:
-        lib = A.load_library()
-        b = self._pod()
-        n = int(lib.smc_galerkin_n_basis(C.byref(b)))
-        if n < 0:
-            _check(lib.smc_galerkin_modes(C.byref(b), None))
-        out = np.zeros((n, 2), dtype=np.int32)
-        _check(lib.smc_galerkin_modes(C.byref(b), out.ctypes.data_as(C.POINTER(C.c_int32))))
-        return [(int(a), int(c)) for a, c in out]
-
-
-@dataclass
-class GalerkinResult:
-    """GalerkinResult (galerkin.hpp:20-27)."""
-    observation_values: np.ndarray
-    coefficients_at_observations: np.ndarray | None
-    final_coefficients: np.ndarray
-    basis_modes: list
-    dt_used: float
-    steps: int
-
-
-def _basis(basis) -> GalerkinBasis:
-    return basis if isinstance(basis, GalerkinBasis) else GalerkinBasis("box", int(basis))
-
-
-def galerkin_spectral_radius(spec: AdProblemSpec, basis, ctx: Context | None = None) -> float:
-    """galerkin_spectral_radius (galerkin.cpp:151-157)."""
-    ctx = ctx or default_context()
-    p, keep = spec._pod()
-    b = _basis(basis)._pod()
-    out = C.c_double()
-    _check(ctx.lib.smc_galerkin_spectral_radius(ctx.handle, C.byref(p), C.byref(b), C.byref(out)))
-    return out.value
-
-
-def galerkin_solve_ad(spec: AdProblemSpec, basis, dt_ref: float, keep_observation_coefficients: bool = False,
-                      ctx: Context | None = None) -> GalerkinResult:
-    """galerkin_solve_ad (galerkin.hpp:36-40, galerkin.cpp:159-231) on the
-    device; `basis` is a GalerkinBasis or a box cutoff (the int overload)."""
-    ctx = ctx or default_context()
-    b = _basis(basis)
-    modes = b.modes()
-    nb = len(modes)
-    p, keep = spec._pod()
-    vals = np.zeros(len(spec.observations))
-    final = np.zeros((nb, 2))
-    cat = np.zeros((len(spec.observations), nb, 2)) if keep_observation_coefficients else None
-    r = A.smc_galerkin_result(A.dptr(vals), A.dptr(cat), A.dptr(final), 0.0, 0)
-    _check(ctx.lib.smc_galerkin_solve_ad(ctx.handle, C.byref(p), C.byref(b._pod()), C.c_double(dt_ref), C.byref(r)))
-    to_c = (lambda a: a[..., 0] + 1j * a[..., 1])
-    return GalerkinResult(vals, to_c(cat) if cat is not None else None, to_c(final), modes, r.dt_used, int(r.steps))
-
-
-def galerkin_field_grid(result: GalerkinResult, n: int, basis=None, ctx: Context | None = None) -> np.ndarray:
-    """galerkin_field_grid (galerkin.cpp:233-250): n x n grid, row-major,
-    x2 fastest (result.basis_modes must be the basis' mode order)."""
-    ctx = ctx or default_context()
-    if basis is None:
-        L = max(max(abs(a), abs(c)) for a, c in result.basis_modes)
-        box = len(result.basis_modes) == (2 * L + 1) ** 2
-        basis = GalerkinBasis("box" if box else "disk", L)
-    b = _basis(basis)._pod()
-    c = np.ascontiguousarray(np.stack([result.final_coefficients.real, result.final_coefficients.imag], axis=-1))
-    out = np.zeros(int(n) * int(n)) if n >= 2 else np.zeros(1)
-    _check(ctx.lib.smc_galerkin_field_grid(ctx.handle, C.byref(b), A.dptr(c), int(n), A.dptr(out)))
-    return out
+# The callers above the forward maps live in their own modules (mirroring the
+# reference's inference / optimize / galerkin headers); re-exported here.
+from .inference import (ChainConfig, LikelihoodSpec, PriorSpec, prior_draw, run_chains,  # noqa: E402,F401
+                        velocity_from_coefficients)
+from .optimize import (ForcingBasis, ForcingControl, NelderMeadOptions, _control_spec, forcing_basis,  # noqa: E402,F401
+                       forcing_cost, nelder_mead, optimize_forcing)
+from .galerkin import (GalerkinBasis, GalerkinResult, galerkin_field_grid, galerkin_solve_ad,  # noqa: E402,F401
+                       galerkin_spectral_radius)
