@@ -8,6 +8,7 @@
 // (bvp_disk.cu).
 #pragma once
 
+#include <type_traits>
 #include <utility>
 
 #include "disk_shape.h"
@@ -77,18 +78,37 @@ __device__ __forceinline__ void disk_row_pairs(const SmemCoef<T>& C, const Power
     (disk_pair<K, K1, Js + 1, T, P>(C, W, a), ...);
 }
 
+// Harmonics e^{i k theta} for k = 2..K.  FP64: the Chebyshev recurrence
+// X_k = 2 cos(theta) X_{k-1} - X_{k-2} (2 DFMA per k instead of the 4 of a
+// complex multiply; rounding error grows like eps k^2 — 1e-14 at k = 12,
+// 1e-12 at k = 80, far inside the 1e-10 parity gate).  FP32 keeps the complex
+// product (eps k^2 would be 4e-4 at k = 80).
+template <class T>
+constexpr bool kChebyshev = std::is_same<T, double>::value;
+
 // Row k1 >= 1: P1 <- P1 e1 (k1 > 1), row sums A and B', then
-//   v2 += k1 Re(P1 A),  v1 -= Re(P1 B').
+//   v2 += k1 Re(P1 A),  v1 -= Re(P1 B').  (q1r, q1i) = P1[k1 - 1] for the
+//   recurrence, tc1 = 2 cos(theta1).
 template <int K, int K1, class T, int P>
 __device__ __forceinline__ void disk_row(const SmemCoef<T>& C, const Powers<K, T, P>& W, const T (&c1)[P],
-                                         const T (&s1)[P], T (&p1r)[P], T (&p1i)[P], T (&acc1)[P], T (&acc2)[P]) {
+                                         const T (&s1)[P], const T (&tc1)[P], T (&p1r)[P], T (&p1i)[P],
+                                         T (&q1r)[P], T (&q1i)[P], T (&acc1)[P], T (&acc2)[P]) {
     using S = DiskShape<K>;
     if constexpr (K1 > 1) {
 #pragma unroll
         for (int p = 0; p < P; ++p) {
-            const T nr = fma(p1r[p], c1[p], -p1i[p] * s1[p]);
-            p1i[p] = fma(p1r[p], s1[p], p1i[p] * c1[p]);
-            p1r[p] = nr;
+            if constexpr (kChebyshev<T>) {
+                const T nr = fma(tc1[p], p1r[p], -q1r[p]);
+                const T ni = fma(tc1[p], p1i[p], -q1i[p]);
+                q1r[p] = p1r[p];
+                q1i[p] = p1i[p];
+                p1r[p] = nr;
+                p1i[p] = ni;
+            } else {
+                const T nr = fma(p1r[p], c1[p], -p1i[p] * s1[p]);
+                p1i[p] = fma(p1r[p], s1[p], p1i[p] * c1[p]);
+                p1r[p] = nr;
+            }
         }
     }
     T g0r, g0i;
@@ -113,13 +133,16 @@ template <int K, class T, int P, int... K1s>
 __device__ __forceinline__ void disk_rows(const SmemCoef<T>& C, const Powers<K, T, P>& W, const T (&c1)[P],
                                           const T (&s1)[P], T (&acc1)[P], T (&acc2)[P],
                                           std::integer_sequence<int, K1s...>) {
-    T p1r[P], p1i[P];
+    T p1r[P], p1i[P], q1r[P], q1i[P], tc1[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) {
         p1r[p] = c1[p];
         p1i[p] = s1[p];
+        q1r[p] = T(1);
+        q1i[p] = T(0);
+        tc1[p] = T(2) * c1[p];
     }
-    (disk_row<K, K1s + 1, T, P>(C, W, c1, s1, p1r, p1i, acc1, acc2), ...);
+    (disk_row<K, K1s + 1, T, P>(C, W, c1, s1, tc1, p1r, p1i, q1r, q1i, acc1, acc2), ...);
 }
 
 // Row k1 = 0: modes (0, j) only (g- = 0), P1 = 1: v1 = -sum (g_re qr - g_im qs).
@@ -158,12 +181,25 @@ __device__ __forceinline__ void velocity_disk(const SmemCoef<T>& C, const T (&x1
         sincospi_t(T(2) * x2[p], &s2, &c2);
         W.pr[p][1] = c2;
         W.pi[p][1] = s2;
-        // P2[j] = P2[j/2] P2[j - j/2]: dependency depth log2(K) instead of K
+        if constexpr (kChebyshev<T>) {
+            const T tc = T(2) * c2;
+            T rm = T(1), im = T(0);  // P2[j - 2]
 #pragma unroll
-        for (int j = 2; j <= K; ++j) {
-            const int a = j / 2, b = j - j / 2;
-            W.pr[p][j] = fma(W.pr[p][a], W.pr[p][b], -W.pi[p][a] * W.pi[p][b]);
-            W.pi[p][j] = fma(W.pr[p][a], W.pi[p][b], W.pi[p][a] * W.pr[p][b]);
+            for (int j = 2; j <= K; ++j) {
+                const T nr = fma(tc, W.pr[p][j - 1], -rm), ni = fma(tc, W.pi[p][j - 1], -im);
+                rm = W.pr[p][j - 1];
+                im = W.pi[p][j - 1];
+                W.pr[p][j] = nr;
+                W.pi[p][j] = ni;
+            }
+        } else {
+            // P2[j] = P2[j/2] P2[j - j/2]: dependency depth log2(K) instead of K
+#pragma unroll
+            for (int j = 2; j <= K; ++j) {
+                const int a = j / 2, b = j - j / 2;
+                W.pr[p][j] = fma(W.pr[p][a], W.pr[p][b], -W.pi[p][a] * W.pi[p][b]);
+                W.pi[p][j] = fma(W.pr[p][a], W.pi[p][b], W.pi[p][a] * W.pr[p][b]);
+            }
         }
         W.qr[p][1] = c2;
         W.qi[p][1] = s2;

@@ -103,7 +103,10 @@ class DeviceOps:
         return sums
 
     def divide(self, sums, n: int):
-        return sums / float(n)  # IEEE division, same as executor.cpp:103
+        # IEEE division, as executor.cpp:103.  Tensor / tensor: dividing by a
+        # Python scalar lets ATen multiply by the rounded reciprocal instead,
+        # which is off by an ulp for some sums.
+        return sums / self.torch.full_like(sums, float(n))
 
     def all_gather(self, local, counts: list[int]):
         """Rank-ordered concatenation of every rank's [n_obs][count_r] chunk
