@@ -16,7 +16,7 @@
 
 namespace smc {
 
-__device__ __forceinline__ double log_t(double x) { return fm::log_pos(x); }  // x = uniform in (0,1)
+__device__ __forceinline__ double log_t(double x) { return fm::log_tab(x); }  // x = uniform in (0,1)
 __device__ __forceinline__ float log_t(float x) { return __logf(x); }
 
 // Particles local[p] (p < P) of observation `obs`; entries >= span are

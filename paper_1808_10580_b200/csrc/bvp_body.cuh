@@ -28,7 +28,7 @@ namespace smc {
 
 constexpr int kBvpBlock = 128;
 
-__device__ __forceinline__ double log_u(double x) { return fm::log_pos(x); }  // uniform in (0,1)
+__device__ __forceinline__ double log_u(double x) { return fm::log_tab(x); }  // uniform in (0,1)
 __device__ __forceinline__ float log_u(float x) { return __logf(x); }
 __device__ __forceinline__ double sqrt_u(double v) { return fm::sqrt_pos(v); }
 __device__ __forceinline__ float sqrt_u(float v) { return sqrtf(v); }

@@ -26,7 +26,7 @@ __global__ void normal_pairs_kernel(uint64_t seed, uint32_t obs, uint32_t partic
     if (i >= n) return;
     const Uniform2 u = uniform_block(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32), obs, particle,
                                      static_cast<uint64_t>(i));
-    const double r = fm::sqrt_pos(-2.0 * fm::log_pos(u.u0));
+    const double r = fm::sqrt_pos(-2.0 * fm::log_tab(u.u0));
     double sn, cs;
     fm::sincospi(2.0 * u.u1, &sn, &cs);
     out[2 * i] = r * cs;

@@ -11,6 +11,9 @@ void fm_sincospi(const double* a, int64_t n, double* s, double* c) {
 void fm_log(const double* x, int64_t n, double* y) {
     for (int64_t i = 0; i < n; ++i) y[i] = smc::fm::log_pos(x[i]);
 }
+void fm_log_tab(const double* x, int64_t n, double* y) {
+    for (int64_t i = 0; i < n; ++i) y[i] = smc::fm::log_tab(x[i]);
+}
 void fm_exp(const double* x, int64_t n, double* y) {
     for (int64_t i = 0; i < n; ++i) y[i] = smc::fm::exp_(x[i]);
 }

@@ -22,7 +22,8 @@ def fm(tmp_path_factory):
                     str(ROOT / "tests/cpp/fastmath_host.cpp")], check=True)
     lib = C.CDLL(str(out))
     P = C.POINTER(C.c_double)
-    for name, n in [("fm_sincospi", 4), ("fm_log", 3), ("fm_exp", 3), ("fm_sqrt", 3), ("fm_div", 4)]:
+    for name, n in [("fm_sincospi", 4), ("fm_log", 3), ("fm_log_tab", 3), ("fm_exp", 3), ("fm_sqrt", 3),
+                    ("fm_div", 4)]:
         getattr(lib, name).restype = None
     return lib
 
@@ -72,6 +73,24 @@ def test_log_on_uniforms(fm):
     y = np.empty_like(x)
     fm.fm_log(_p(x), C.c_int64(x.size), _p(y))
     assert ulp_err(y, [mpmath.log(mpmath.mpf(v)) for v in x]) <= 2.0
+
+
+def test_table_log_on_uniforms(fm):
+    """fm::log_tab, the particle kernels' Box-Muller log: <= 1.5 ulp (1.37
+    measured over 2e5 uniforms; two roundings in hi + (lo + p)), including
+    x -> 1 from below (relative accuracy kept by the c = 1 bins) and tiny x."""
+    x = np.concatenate([RNG.uniform(0, 1, 4000), 2.0 ** -RNG.uniform(1, 54, 1000),
+                        1 - 2.0 ** -RNG.uniform(8, 53, 500), 1 - RNG.uniform(0, 1e-3, 500),
+                        [2.0 ** -54, 0.5, 1 - 2.0 ** -53, np.sqrt(0.5), 0.7071067811865476, 1.4140625 / 2,
+                         (1 + 53 / 128) / 2 - 2.0 ** -53, 0.99609375, 0.9921875]])
+    y = np.empty_like(x)
+    fm.fm_log_tab(_p(x), C.c_int64(x.size), _p(y))
+    assert ulp_err(y, [mpmath.log(mpmath.mpf(v)) for v in x]) <= 1.5
+    for g in (1.0, 2.0, 3.5, 1e10, 1e-300):  # general normal x
+        v = np.array([g])
+        w = np.empty_like(v)
+        fm.fm_log_tab(_p(v), C.c_int64(1), _p(w))
+        assert ulp_err(w, [mpmath.log(mpmath.mpf(g))]) <= 1.0
 
 
 def test_exp(fm):
