@@ -90,14 +90,22 @@ __global__ void pcn_propose_kernel(PcnStep S) {
         Up[2 * i + 1] = S.contraction * U[2 * i + 1] + S.beta * x2;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double acc = 0.0;
-        for (int64_t i = 0; i < S.dim; ++i) {
-            const double r = Up[i] / S.stds[i >> 1];
-            acc += r * r;
+    // prior norm: the squares in parallel, the sum in the reference's order
+    // (one thread, shared-memory chunks) so the norm is bit-identical
+    __shared__ double sq[1024];
+    double acc = 0.0;
+    for (int64_t base = 0; base < S.dim; base += 1024) {
+        const int64_t n = S.dim - base < 1024 ? S.dim - base : 1024;
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+            const double r = Up[base + i] / S.stds[(base + i) >> 1];
+            sq[i] = r * r;
         }
-        S.norm_prop[b] = 0.5 * acc;
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int64_t i = 0; i < n; ++i) acc += sq[i];
+        __syncthreads();
     }
+    if (threadIdx.x == 0) S.norm_prop[b] = 0.5 * acc;
 }
 
 // velocity_from_coefficients -> coefficient blocks through the host-built
