@@ -435,3 +435,16 @@ def test_bvp_ragged_with_failures(ctx, port, n):
         return
     got = S.observe_bvp(spec, 606, ctx=ctx)
     assert_estimates(got, list(want), 1.0)
+
+
+def test_milstein_equals_euler_maruyama_for_isotropic_diffusion(ctx):
+    """milstein_step returns em_step for isotropic diffusion (sde.cpp:18-22):
+    the scheme flag must not change a single bit."""
+    spec = specs.c1_two_mode(n_particles=2000)
+    em = S.observe_ad(spec, 7, ctx=ctx)
+    spec.scheme = S.StepScheme.milstein
+    assert S.observe_ad(spec, 7, ctx=ctx) == em
+    bvp = specs.paper_bvp(n_particles=500)
+    em_b = S.observe_bvp(bvp, 606, ctx=ctx)
+    bvp.scheme = S.StepScheme.milstein
+    assert S.observe_bvp(bvp, 606, ctx=ctx) == em_b
