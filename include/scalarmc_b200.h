@@ -217,7 +217,9 @@ smc_status smc_bvp_forcing_basis(smc_ctx* ctx, const smc_bvp_problem* prob, uint
  * device.  Chain c uses the stream NormalStream{chain_seeds[c], 0xFFFFFFFF, 0}
  * exactly as run_chain does with config.seed (inference.cpp:12, :175), so
  * chain c reproduces run_chain(config with seed = chain_seeds[c]).
- * `forward` is the likelihood's AdProblemSpec (its velocity slot is ignored);
+ * `forward` is the likelihood's AdProblemSpec (its velocity slot is ignored),
+ * or NULL for run_chain(..., likelihood = nullptr): Phi == 0, every proposal
+ * accepted, no forward map (data / noise_std / forward_seed unused);
  * data: [n_obs] (LikelihoodSpec::data); u0: [n_chains][dim] or NULL (draw from
  * the prior).  Output arrays are caller-owned; any may be NULL except
  * final_u. */

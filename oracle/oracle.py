@@ -234,7 +234,7 @@ class Reference(_Checker):
                   workers: int = 0) -> dict:
         """The reference's run_chain (inference.cpp:170-194) with LikelihoodSpec
         `like` (paper_1808_10580_b200.LikelihoodSpec)."""
-        p, keep = like.forward._pod()
+        p, keep = like.forward._pod() if like is not None else (None, None)
         dim = prior.dimension()
         n_samples = max(0, (n_steps - max(burn_in, 0) - 1) // thin + 1) if n_steps > burn_in else 0
         trace = np.zeros(max(n_steps, 1))
@@ -242,10 +242,11 @@ class Reference(_Checker):
         final_u = np.zeros(dim)
         map_u = np.zeros(dim)
         sc = np.zeros(3)
-        d = np.ascontiguousarray(like.data, dtype=np.float64)
+        d = np.ascontiguousarray(like.data if like is not None else [0.0], dtype=np.float64)
         u0p = np.ascontiguousarray(u0, dtype=np.float64).ctypes.data_as(_dp) if u0 is not None else _dp()
-        rc = self.lib.ref_run_chain(C.byref(p), C.byref(prior._pod()), d.ctypes.data_as(_dp),
-                                    C.c_double(like.noise_std), C.c_uint64(like.forward_seed), C.c_int64(n_steps),
+        rc = self.lib.ref_run_chain(C.byref(p) if p is not None else None, C.byref(prior._pod()),
+                                    d.ctypes.data_as(_dp), C.c_double(like.noise_std if like is not None else 1.0),
+                                    C.c_uint64(like.forward_seed if like is not None else 0), C.c_int64(n_steps),
                                     C.c_double(beta), C.c_int64(burn_in), C.c_int64(thin), C.c_uint64(seed), u0p,
                                     C.c_int(workers), trace.ctypes.data_as(_dp), samples.ctypes.data_as(_dp),
                                     final_u.ctypes.data_as(_dp), map_u.ctypes.data_as(_dp), sc.ctypes.data_as(_dp))

@@ -288,11 +288,13 @@ int ref_misfit(const smc_ad_problem* base, const smc_prior* prior, const double*
     return guarded([&] {
         const PriorSpec ps{prior->cutoff, prior->s0, prior->alpha};
         LikelihoodSpec like;
-        like.forward = to_ad(*base);
-        like.data.assign(data, data + base->n_obs);
-        like.noise_std = noise_std;
-        like.forward_seed = forward_seed;
-        like.workers = workers;
+        if (base) {  // base == nullptr: run_chain(..., likelihood = nullptr) — Phi == 0
+            like.forward = to_ad(*base);
+            like.data.assign(data, data + base->n_obs);
+            like.noise_std = noise_std;
+            like.forward_seed = forward_seed;
+            like.workers = workers;
+        }
         *out = like.misfit(ps, std::span<const double>(u, static_cast<std::size_t>(ps.dimension())));
     });
 }
@@ -326,11 +328,13 @@ int ref_run_chain(const smc_ad_problem* base, const smc_prior* prior, const doub
     return guarded([&] {
         const PriorSpec ps{prior->cutoff, prior->s0, prior->alpha};
         LikelihoodSpec like;
-        like.forward = to_ad(*base);
-        like.data.assign(data, data + base->n_obs);
-        like.noise_std = noise_std;
-        like.forward_seed = forward_seed;
-        like.workers = workers;
+        if (base) {  // base == nullptr: run_chain(..., likelihood = nullptr) — Phi == 0
+            like.forward = to_ad(*base);
+            like.data.assign(data, data + base->n_obs);
+            like.noise_std = noise_std;
+            like.forward_seed = forward_seed;
+            like.workers = workers;
+        }
         ChainConfig cc;
         cc.n_steps = n_steps;
         cc.beta = beta;
@@ -340,7 +344,7 @@ int ref_run_chain(const smc_ad_problem* base, const smc_prior* prior, const doub
         std::optional<std::vector<double>> start;
         const std::size_t dim = static_cast<std::size_t>(ps.dimension());
         if (u0) start = std::vector<double>(u0, u0 + dim);
-        const ChainResult r = run_chain(cc, ps, &like, start);
+        const ChainResult r = run_chain(cc, ps, base ? &like : nullptr, start);
         for (std::size_t i = 0; i < r.phi_trace.size(); ++i) phi_trace[i] = r.phi_trace[i];
         for (std::size_t k = 0; k < r.samples.size(); ++k)
             for (std::size_t i = 0; i < dim; ++i) samples[k * dim + i] = r.samples[k][i];

@@ -100,17 +100,22 @@ smc_status smc_pcn_chains(smc_ctx* ctx, const smc_ad_problem* forward, const smc
         if (prior->cutoff < 1) raise(SMC_EINVAL, "PriorSpec: cutoff must be >= 1");
         if (!(prior->s0 >= 0.0)) raise(SMC_EINVAL, "PriorSpec: s0 must be >= 0");
         if (!std::isfinite(prior->alpha)) raise(SMC_EINVAL, "PriorSpec: alpha must be finite");
-        if (!(noise_std > 0.0)) raise(SMC_EINVAL, "LikelihoodSpec: noise_std must be positive");
+        // forward == nullptr: run_chain(..., likelihood = nullptr) — Phi == 0, no forward map
+        const bool prior_only = forward == nullptr;
+        if (!prior_only && !(noise_std > 0.0)) raise(SMC_EINVAL, "LikelihoodSpec: noise_std must be positive");
         if (cfg->n_steps > 0 && !(cfg->beta > 0.0 && cfg->beta <= 1.0))
             raise(SMC_EINVAL, "pcn_step: beta must be in (0,1]");
         if (n_chains < 1) raise(SMC_EINVAL, "pcn_chains: need at least one chain");
         if (!out || !out->final_u) raise(SMC_EINVAL, "pcn_chains: final_u output is required");
-        smc_ad_problem p = *forward;
-        check_kappa(p.kappa);
-        check_scalar(p.initial_condition);
-        ad_validate(p);
-        check_particle_range(p.n_particles);
-        if (p.precision == SMC_FP64_STRICT) raise(SMC_EINVAL, "strict precision is single-sample only");
+        smc_ad_problem p{};
+        if (!prior_only) {
+            p = *forward;
+            check_kappa(p.kappa);
+            check_scalar(p.initial_condition);
+            ad_validate(p);
+            check_particle_range(p.n_particles);
+            if (p.precision == SMC_FP64_STRICT) raise(SMC_EINVAL, "strict precision is single-sample only");
+        }
         cudaStream_t s = ctx->stream;
         const int64_t n_obs = p.n_obs, n = p.n_particles, B = n_chains;
 
@@ -129,7 +134,7 @@ smc_status smc_pcn_chains(smc_ctx* ctx, const smc_ad_problem* forward, const smc
         const LatticeHost Lh = lattice_structure(structure);
         const PackMap pmap = pack_map(prior->cutoff, use_disk, &Lh);
         const int64_t stride = pmap.stride;
-        if (static_cast<int64_t>(p.n_obs) <= 0) raise(SMC_EINVAL, "AdProblemSpec: no observations");
+        if (!prior_only && static_cast<int64_t>(p.n_obs) <= 0) raise(SMC_EINVAL, "AdProblemSpec: no observations");
 
         // device buffers (freed at the end of the call)
         std::vector<void*> owned;
@@ -157,15 +162,15 @@ smc_status smc_pcn_chains(smc_ctx* ctx, const smc_ad_problem* forward, const smc
         S.n_steps = cfg->n_steps;
         S.n_samples = n_samples;
         S.noise_std = noise_std;
-        S.noise_inf = std::isinf(noise_std) ? 1 : 0;
+        S.noise_inf = (prior_only || std::isinf(noise_std)) ? 1 : 0;
         auto* d_stds = static_cast<double*>(dalloc(8 * M));
         h2d(d_stds, stds.data(), 8 * M);
         S.stds = d_stds;
         auto* d_seeds = static_cast<uint64_t*>(dalloc(8 * B));
         h2d(d_seeds, chain_seeds, 8 * B);
         S.seeds = d_seeds;
-        auto* d_data = static_cast<double*>(dalloc(8 * n_obs));
-        h2d(d_data, data, 8 * n_obs);
+        auto* d_data = static_cast<double*>(dalloc(8 * std::max<int64_t>(n_obs, 1)));
+        if (!prior_only) h2d(d_data, data, 8 * n_obs);
         S.data = d_data;
         const PackDev pdev = upload_pack_map(ctx, pmap);
         S.U = static_cast<double*>(dalloc(8 * B * dim));
@@ -187,18 +192,23 @@ smc_status smc_pcn_chains(smc_ctx* ctx, const smc_ad_problem* forward, const smc
 
         // forward image (theta_0, observations, lattice tiles); coefficient
         // blocks come from the pack kernel
-        p.velocity.is_constant = 0;
-        p.velocity.max_wavenumber = prior->cutoff;
-        AdPrepared P = prepare_ad(ctx, p, {&structure}, structure, 0, n_obs);
-        P.L.seed = forward_seed;
-        P.L.seeds = nullptr;
-        if (!use_disk) {
-            P.L.vel.lat.coef = d_blocks;
-            P.L.vel.lat.sample_stride = stride;
+        AdPrepared P{};
+        double* values = nullptr;
+        if (!prior_only) {
+            p.velocity.is_constant = 0;
+            p.velocity.max_wavenumber = prior->cutoff;
+            P = prepare_ad(ctx, p, {&structure}, structure, 0, n_obs);
+            P.L.seed = forward_seed;
+            P.L.seeds = nullptr;
+            if (!use_disk) {
+                P.L.vel.lat.coef = d_blocks;
+                P.L.vel.lat.sample_stride = stride;
+            }
+            values = ctx->values.get<double>(static_cast<size_t>(B * n_obs * n));
         }
-        double* values = ctx->values.get<double>(static_cast<size_t>(B * n_obs * n));
 
         auto forward_map = [&]() -> smc_estimate* {
+            if (prior_only) return nullptr;  // Phi == 0 (noise_inf), nothing to evaluate
             for (int64_t b0 = 0; b0 < B; b0 += 65535)
                 CK(launch_pack(pdev, S.Up + b0 * dim, dim, std::min<int64_t>(65535, B - b0), d_blocks + b0 * stride,
                                nullptr, s));

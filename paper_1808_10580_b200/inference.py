@@ -117,7 +117,7 @@ class ChainConfig:
     seed: int = 0
 
 
-def run_chains(config: ChainConfig, prior: PriorSpec, likelihood: LikelihoodSpec, seeds: Sequence[int],
+def run_chains(config: ChainConfig, prior: PriorSpec, likelihood: LikelihoodSpec | None, seeds: Sequence[int],
                u0: np.ndarray | None = None, keep_samples: bool = True, keep_trace: bool = True,
                ctx: Context | None = None) -> dict:
     """len(seeds) independent pCN chains on the device (run_chain,
@@ -127,8 +127,11 @@ def run_chains(config: ChainConfig, prior: PriorSpec, likelihood: LikelihoodSpec
     map_objective [B], accepted [B], acceptance_rate [B], phi_trace
     [B][n_steps], samples [B][n_samples][dim]."""
     ctx = ctx or default_context()
-    likelihood.validate()
-    p, keep = likelihood.forward._pod()
+    if likelihood is not None:
+        likelihood.validate()
+        p, keep = likelihood.forward._pod()
+    else:  # run_chain(..., likelihood = nullptr): Phi == 0
+        p, keep = None, None
     seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
     B, dim = len(seeds), prior.dimension()
     cfg = A.smc_chain_config(config.n_steps, config.beta, config.burn_in, config.thin)
@@ -140,10 +143,12 @@ def run_chains(config: ChainConfig, prior: PriorSpec, likelihood: LikelihoodSpec
     out = A.smc_chain_outputs(A.dptr(res["final_u"]), A.dptr(res["final_phi"]), A.dptr(res["map_u"]),
                               A.dptr(res["map_objective"]), res["accepted"].ctypes.data_as(C.POINTER(C.c_int64)),
                               A.dptr(res["phi_trace"]), A.dptr(res["samples"]))
-    d = np.ascontiguousarray(likelihood.data, dtype=np.float64)
+    d = np.ascontiguousarray(likelihood.data if likelihood is not None else [0.0], dtype=np.float64)
     u0p = A.dptr(np.ascontiguousarray(u0, dtype=np.float64).reshape(B, dim)) if u0 is not None else A.dptr(None)
-    _check(ctx.lib.smc_pcn_chains(ctx.handle, C.byref(p), C.byref(prior._pod()), A.dptr(d),
-                                  C.c_double(likelihood.noise_std), C.c_uint64(likelihood.forward_seed), B,
+    noise = likelihood.noise_std if likelihood is not None else 1.0
+    fseed = likelihood.forward_seed if likelihood is not None else 0
+    _check(ctx.lib.smc_pcn_chains(ctx.handle, C.byref(p) if p is not None else None, C.byref(prior._pod()),
+                                  A.dptr(d), C.c_double(noise), C.c_uint64(fseed), B,
                                   seeds.ctypes.data_as(C.POINTER(C.c_uint64)), u0p, C.byref(cfg), C.byref(out)))
     if keep_trace:
         res["phi_trace"] = res["phi_trace"][:, : config.n_steps]
