@@ -1,6 +1,6 @@
 """The reference's own acceptance criteria (tests/acceptance.cpp of scalarmc)
 run on the B200 path, with the reference's configurations, seeds and
-tolerances.  Criteria covered elsewhere: 1 heat (test_gpu_parity
+tolerances: 2, 4, 7, 8, 9 here.  Criteria covered elsewhere: 1 heat (test_gpu_parity
 test_heat_matches_reference_and_analytic), 3 manufactured Dirichlet
 (test_bvp_manufactured_solution), 5 Milstein == EM
 (test_milstein_equals_euler_maruyama_for_isotropic_diffusion), 6 determinism
@@ -80,3 +80,33 @@ def test_criterion8_pcn_preserves_the_prior(ctx, reference):
     ref = reference.run_chain(None, prior, 2000, 0.8, 0, 1, 888)
     assert ref["accepted"] == 2000
     assert np.allclose(samples[:2000], ref["samples"], rtol=0, atol=1e-12)
+
+
+def test_criterion9_bayesian_recovery(ctx):
+    """acceptance.cpp:236-291: synthetic truth u* from the prior (stream
+    424242/0/0), data = the fixed-seed forward map at u* + 0.05 noise (stream
+    424242/1/0), 200 000 pCN steps (beta 0.12, burn-in 20 000, thin 20, seed
+    31337): the central 95 % posterior interval covers u* in >= 90 % of the
+    components."""
+    prior = S.PriorSpec(2, 0.6, 2.5)
+    forward = S.AdProblemSpec(
+        diffusion=S.DiffusionModel.isotropic(0.05),
+        initial_condition=S.ScalarField.cosine_series([(1.0, (2 * PI, 0.0), 0.0), (0.8, (0.0, 2 * PI), 0.0),
+                                                       (0.6, (2 * PI, 2 * PI), 0.0)]),
+        observations=[S.AdObservation(t, S.Vec2(*x)) for t in (0.06, 0.12, 0.18)
+                      for x in ((0.25, 0.25), (0.75, 0.5), (0.5, 0.75))],
+        n_particles=160, dt=6e-3)
+    truth = S.prior_draw(prior, 424242, 0, 0, ctx)
+    data_spec = S.AdProblemSpec(**{**forward.__dict__})
+    data_spec.velocity = S.VelocityField.fourier(S.velocity_from_coefficients(prior, truth))
+    clean = S.observe_ad(data_spec, 1234, ctx=ctx)
+    noise = S.normal_pairs_device(424242, 1, 0, 5, ctx).reshape(-1)  # normal(): pairs in order
+    data = [e.mean + 0.05 * z for e, z in zip(clean, noise)]
+    like = S.LikelihoodSpec(data=data, noise_std=0.05, forward=forward, forward_seed=1234)
+    cfg = S.ChainConfig(n_steps=200000, beta=0.12, burn_in=20000, thin=20)
+    res = S.run_chains(cfg, prior, like, [31337], keep_trace=False, ctx=ctx)
+    samples = np.sort(res["samples"][0], axis=0)
+    lo = samples[int(0.025 * len(samples))]
+    hi = samples[min(int(0.975 * len(samples)), len(samples) - 1)]
+    covered = np.sum((truth >= lo) & (truth <= hi))
+    assert covered / prior.dimension() >= 0.90, (covered, prior.dimension(), res["acceptance_rate"])
