@@ -63,7 +63,11 @@ __device__ __forceinline__ void ad_particles_p(const AdLaunch& L, int obs, int s
             xi2[p] = nx2[p];
         }
         draw(step + 1, nx1, nx2);  // one block past the last step is drawn and discarded
-        velocity(x1, x2, v1, v2);
+        // `zero` is 0 for every reachable step but depends on the (uniform)
+        // step counter, so constant-bank coefficient reads indexed by it
+        // cannot be hoisted out of the loop (see ad_disk.cu ConstCoef)
+        const int zero = static_cast<int>(static_cast<uint64_t>(step) >> 62);
+        velocity(x1, x2, v1, v2, zero);
         const bool last = step + 1 == n;
         const T h = last ? dt_last : dt;
         const T s = last ? sr_last : sr;
@@ -86,9 +90,10 @@ template <class T, class Vel>
 __device__ __forceinline__ void ad_particle(const AdLaunch& L, int obs, int sample, int64_t local, int64_t span,
                                             Vel&& velocity) {
     const int64_t loc[1] = {local};
-    ad_particles_p<T, 1>(L, obs, sample, loc, span, [&](const T (&x1)[1], const T (&x2)[1], T (&v1)[1], T (&v2)[1]) {
-        velocity(x1[0], x2[0], v1[0], v2[0]);
-    });
+    ad_particles_p<T, 1>(L, obs, sample, loc, span,
+                         [&](const T (&x1)[1], const T (&x2)[1], T (&v1)[1], T (&v2)[1], int) {
+                             velocity(x1[0], x2[0], v1[0], v2[0]);
+                         });
 }
 
 }  // namespace smc

@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <cstring>
 #include <utility>
 
 #include "ad_body.cuh"
@@ -42,9 +43,77 @@ __global__ void __launch_bounds__(kBlock, MINB) ad_particles_disk(const AdLaunch
 #pragma unroll
     for (int p = 0; p < P; ++p) local[p] = base + static_cast<int64_t>(p) * kBlock;
     ad_particles_p<T, P>(L, obs, sample, local, span,
-                         [&](const T (&x1)[P], const T (&x2)[P], T (&v1)[P], T (&v2)[P]) {
+                         [&](const T (&x1)[P], const T (&x2)[P], T (&v1)[P], T (&v2)[P], int) {
                              velocity_disk<K, T, P>(C, x1, x2, v1, v2);
                          });
+}
+
+// Single-sample launches take the coefficient block as a KERNEL PARAMETER
+// (constant bank 0, per launch, so concurrent contexts cannot race): the
+// DFMAs then read their coefficient through uniform registers (LDCU), which
+// frees the vector register file's operand bandwidth that the shared-memory
+// version spends on it (C2 36.3 -> 31.7 ms).  The loads are indexed by a
+// value that is 0 but varies with the step counter, so ptxas keeps them
+// inside the loop instead of hoisting ~200 coefficients into spilled
+// registers.
+template <int K>
+struct alignas(16) DiskParam {
+    double2 c[DiskShape<K>::n_coef / 2];
+};
+template <int K, class T>
+struct ParamCoef {
+    const DiskParam<K>& P;
+    int zero;  // 0, but loop-variant: keeps the loads inside the step loop
+    template <int O>
+    __device__ __forceinline__ void get2(T& a, T& b) const {
+        const double2 v = P.c[zero + O / 2];
+        a = T(v.x);
+        b = T(v.y);
+    }
+};
+
+template <int K, class T, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) ad_particles_disk_param(const AdLaunch L, const DiskParam<K> P) {
+    const int obs = blockIdx.y;
+    const int64_t span = L.p_end - L.p_begin;
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x;
+    if (base >= span) return;
+    int64_t local[1] = {base};
+    ad_particles_p<T, 1>(L, obs, 0, local, span,
+                         [&](const T (&x1)[1], const T (&x2)[1], T (&v1)[1], T (&v2)[1], int zero) {
+                             const ParamCoef<K, T> C{P, zero};
+                             velocity_disk<K, T, 1>(C, x1, x2, v1, v2);
+                         });
+}
+
+template <int K, class T>
+cudaError_t launch_param(const AdLaunch& L, cudaStream_t s) {
+    static_assert(DiskShape<K>::n_coef % 2 == 0, "coefficient pairs");
+    DiskParam<K> P;
+    std::memcpy(&P, L.host_disk, sizeof(P));
+    const int64_t span = L.p_end - L.p_begin;
+    const dim3 grid(static_cast<unsigned>((span + kBlock - 1) / kBlock), static_cast<unsigned>(L.n_obs), 1);
+    ad_particles_disk_param<K, T, (K <= 8 ? 4 : 3)><<<grid, kBlock, 0, s>>>(L, P);
+    return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t dispatch_param(const AdLaunch& L, int K, cudaStream_t s) {  // T = double
+    switch (K) {
+        case 1: return launch_param<1, T>(L, s);
+        case 2: return launch_param<2, T>(L, s);
+        case 3: return launch_param<3, T>(L, s);
+        case 4: return launch_param<4, T>(L, s);
+        case 5: return launch_param<5, T>(L, s);
+        case 6: return launch_param<6, T>(L, s);
+        case 7: return launch_param<7, T>(L, s);
+        case 8: return launch_param<8, T>(L, s);
+        case 9: return launch_param<9, T>(L, s);
+        case 10: return launch_param<10, T>(L, s);
+        case 11: return launch_param<11, T>(L, s);
+        case 12: return launch_param<12, T>(L, s);
+        default: return cudaErrorNotSupported;
+    }
 }
 
 template <int K, class T, int P, int MINB>
@@ -98,6 +167,12 @@ cudaError_t dispatch(const AdLaunch& L, int K, const double* c, cudaStream_t s) 
 
 cudaError_t launch_ad_disk(const AdLaunch& L, int K, const double* coef, cudaStream_t s) {
     if (L.p_end - L.p_begin <= 0) return cudaSuccess;
+    // one coefficient block with its host copy: the kernel-parameter path
+    // (SMC_DISK_P=2 keeps the shared-memory kernel, which has the P=2 form)
+    const char* pe = std::getenv("SMC_DISK_P");
+    // (FP64 only: FP32 would convert every coefficient on every use)
+    if (L.n_samples == 1 && L.host_disk && L.precision != 1 && !(pe && std::atoi(pe) == 2))
+        return dispatch_param<double>(L, K, s);
     return L.precision == 1 ? dispatch<float>(L, K, coef, s) : dispatch<double>(L, K, coef, s);
 }
 

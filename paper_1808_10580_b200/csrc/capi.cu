@@ -132,6 +132,10 @@ AdPrepared prepare_ad(smc_ctx* ctx, const smc_ad_problem& p, const std::vector<c
         disk_off = im.reserve(nc * fills.size() * sizeof(double));
         for (size_t b = 0; b < fills.size(); ++b)
             disk_fill(structure.K, *fills[b], reinterpret_cast<double*>(im.bytes.data() + disk_off) + b * nc);
+        if (fills.size() == 1) {
+            const double* h = reinterpret_cast<const double*>(im.bytes.data() + disk_off);
+            out.host_disk.assign(h, h + nc);
+        }
     }
     unsigned char* base = ctx->upload(im);
     if (disk) {
@@ -150,6 +154,7 @@ AdPrepared prepare_ad(smc_ctx* ctx, const smc_ad_problem& p, const std::vector<c
     L.n_samples = 1;
     L.precision = p.precision;
     L.sigma = sigma;
+    L.host_disk = out.host_disk.empty() ? nullptr : out.host_disk.data();
     out.n_obs = obs_count;
     return out;
 }

@@ -173,6 +173,7 @@ struct AdPrepared {
     AdLaunch L{};
     int disk_K = 0;                  // > 0: use the compile-time disk kernel
     const double* disk = nullptr;    // its coefficient blocks (device, one per sample)
+    std::vector<double> host_disk;   // host copy of a single-sample block (kernel-parameter path)
     int64_t n_obs = 0;
     int64_t steps_per_particle_sum = 0;  // sum_j n_j
 };

@@ -33,6 +33,7 @@ smc_status smc_ad_observe_batched(smc_ctx* ctx, const smc_ad_problem* base, cons
         const PreparedVelocity structure = prior_structure(prior->cutoff);
         const int64_t dim = 2 * static_cast<int64_t>(structure.modes.size());
         AdPrepared P = prepare_ad(ctx, p, {&structure}, structure, 0, n_obs);
+        P.L.host_disk = nullptr;  // the coefficient blocks come from the pack kernel
         const LatticeHost Lh = lattice_structure(structure);
         const PackMap pmap = pack_map(prior->cutoff, P.disk_K > 0, &Lh);
         const PackDev pdev = upload_pack_map(ctx, pmap);
@@ -198,6 +199,7 @@ smc_status smc_pcn_chains(smc_ctx* ctx, const smc_ad_problem* forward, const smc
             p.velocity.is_constant = 0;
             p.velocity.max_wavenumber = prior->cutoff;
             P = prepare_ad(ctx, p, {&structure}, structure, 0, n_obs);
+            P.L.host_disk = nullptr;  // the coefficient blocks come from the pack kernel
             P.L.seed = forward_seed;
             P.L.seeds = nullptr;
             if (!use_disk) {

@@ -53,8 +53,8 @@ struct RowAcc {
 // One (k1, +/-j) pair, alpha = g(k1,j) + g(k1,-j), beta = g(k1,j) - g(k1,-j):
 //   A  += (ar r - bi s) + i (ai r + br s)
 //   B' += (br qr - ai qs) + i (bi qr + ar qs)
-template <int K, int K1, int J, class T, int P>
-__device__ __forceinline__ void disk_pair(const SmemCoef<T>& C, const Powers<K, T, P>& W, RowAcc<P, T>& a) {
+template <int K, int K1, int J, class T, int P, class CA>
+__device__ __forceinline__ void disk_pair(const CA& C, const Powers<K, T, P>& W, RowAcc<P, T>& a) {
     constexpr int o = 4 * (DiskShape<K>::pair_offset(K1) + J - 1);
     T ar, ai, br, bi;
     C.template get2<o>(ar, ai);
@@ -72,8 +72,8 @@ __device__ __forceinline__ void disk_pair(const SmemCoef<T>& C, const Powers<K, 
     }
 }
 
-template <int K, int K1, class T, int P, int... Js>
-__device__ __forceinline__ void disk_row_pairs(const SmemCoef<T>& C, const Powers<K, T, P>& W, RowAcc<P, T>& a,
+template <int K, int K1, class T, int P, class CA, int... Js>
+__device__ __forceinline__ void disk_row_pairs(const CA& C, const Powers<K, T, P>& W, RowAcc<P, T>& a,
                                                std::integer_sequence<int, Js...>) {
     (disk_pair<K, K1, Js + 1, T, P>(C, W, a), ...);
 }
@@ -89,8 +89,8 @@ constexpr bool kChebyshev = std::is_same<T, double>::value;
 // Row k1 >= 1: P1 <- P1 e1 (k1 > 1), row sums A and B', then
 //   v2 += k1 Re(P1 A),  v1 -= Re(P1 B').  (q1r, q1i) = P1[k1 - 1] for the
 //   recurrence, tc1 = 2 cos(theta1).
-template <int K, int K1, class T, int P>
-__device__ __forceinline__ void disk_row(const SmemCoef<T>& C, const Powers<K, T, P>& W, const T (&c1)[P],
+template <int K, int K1, class T, int P, class CA>
+__device__ __forceinline__ void disk_row(const CA& C, const Powers<K, T, P>& W, const T (&c1)[P],
                                          const T (&s1)[P], const T (&tc1)[P], T (&p1r)[P], T (&p1i)[P],
                                          T (&q1r)[P], T (&q1i)[P], T (&acc1)[P], T (&acc2)[P]) {
     using S = DiskShape<K>;
@@ -129,8 +129,8 @@ __device__ __forceinline__ void disk_row(const SmemCoef<T>& C, const Powers<K, T
     }
 }
 
-template <int K, class T, int P, int... K1s>
-__device__ __forceinline__ void disk_rows(const SmemCoef<T>& C, const Powers<K, T, P>& W, const T (&c1)[P],
+template <int K, class T, int P, class CA, int... K1s>
+__device__ __forceinline__ void disk_rows(const CA& C, const Powers<K, T, P>& W, const T (&c1)[P],
                                           const T (&s1)[P], T (&acc1)[P], T (&acc2)[P],
                                           std::integer_sequence<int, K1s...>) {
     T p1r[P], p1i[P], q1r[P], q1i[P], tc1[P];
@@ -146,8 +146,8 @@ __device__ __forceinline__ void disk_rows(const SmemCoef<T>& C, const Powers<K, 
 }
 
 // Row k1 = 0: modes (0, j) only (g- = 0), P1 = 1: v1 = -sum (g_re qr - g_im qs).
-template <int K, int J, class T, int P>
-__device__ __forceinline__ void disk_row0_term(const SmemCoef<T>& C, const Powers<K, T, P>& W, T (&a0)[P],
+template <int K, int J, class T, int P, class CA>
+__device__ __forceinline__ void disk_row0_term(const CA& C, const Powers<K, T, P>& W, T (&a0)[P],
                                                T (&a1)[P]) {
     T gr, gi;
     C.template get2<DiskShape<K>::row0_offset + 2 * J>(gr, gi);
@@ -158,8 +158,8 @@ __device__ __forceinline__ void disk_row0_term(const SmemCoef<T>& C, const Power
     }
 }
 
-template <int K, class T, int P, int... Js>
-__device__ __forceinline__ void disk_row0(const SmemCoef<T>& C, const Powers<K, T, P>& W, T (&acc1)[P],
+template <int K, class T, int P, class CA, int... Js>
+__device__ __forceinline__ void disk_row0(const CA& C, const Powers<K, T, P>& W, T (&acc1)[P],
                                           std::integer_sequence<int, Js...>) {
     T a0[P], a1[P];
 #pragma unroll
@@ -169,8 +169,8 @@ __device__ __forceinline__ void disk_row0(const SmemCoef<T>& C, const Powers<K, 
     for (int p = 0; p < P; ++p) acc1[p] = a0[p] + a1[p];
 }
 
-template <int K, class T, int P>
-__device__ __forceinline__ void velocity_disk(const SmemCoef<T>& C, const T (&x1)[P], const T (&x2)[P], T (&v1)[P],
+template <int K, class T, int P, class CA>
+__device__ __forceinline__ void velocity_disk(const CA& C, const T (&x1)[P], const T (&x2)[P], T (&v1)[P],
                                               T (&v2)[P]) {
     T s1[P], c1[P];
     Powers<K, T, P> W;

@@ -31,6 +31,7 @@ struct AdLaunch {
     int32_t precision;         // smc_precision
     double sigma;              // sqrt(2 kappa)
     double* values;            // [n_samples][n_obs][p_end - p_begin]
+    const double* host_disk;   // host copy of the single-sample disk coefficient block (or null)
 };
 
 cudaError_t launch_ad_particles(const AdLaunch& L, cudaStream_t s);
