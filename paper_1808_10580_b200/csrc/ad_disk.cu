@@ -56,22 +56,6 @@ __global__ void __launch_bounds__(kBlock, MINB) ad_particles_disk(const AdLaunch
 // value that is 0 but varies with the step counter, so ptxas keeps them
 // inside the loop instead of hoisting ~200 coefficients into spilled
 // registers.
-template <int K>
-struct alignas(16) DiskParam {
-    double2 c[DiskShape<K>::n_coef / 2];
-};
-template <int K, class T>
-struct ParamCoef {
-    const DiskParam<K>& P;
-    int zero;  // 0, but loop-variant: keeps the loads inside the step loop
-    template <int O>
-    __device__ __forceinline__ void get2(T& a, T& b) const {
-        const double2 v = P.c[zero + O / 2];
-        a = T(v.x);
-        b = T(v.y);
-    }
-};
-
 template <int K, class T, int MINB>
 __global__ void __launch_bounds__(kBlock, MINB) ad_particles_disk_param(const AdLaunch L, const DiskParam<K> P) {
     const int obs = blockIdx.y;

@@ -39,6 +39,29 @@ __device__ __forceinline__ void SmemCoef<float>::get2(float& a, float& b) const 
     asm volatile("ld.shared.v2.f32 {%0, %1}, [%2+%3];" : "=f"(a), "=f"(b) : "r"(base), "n"(O * 4));
 }
 
+// Coefficient block passed BY VALUE as a kernel parameter (constant bank 0):
+// the DFMAs then take each coefficient from a uniform register (LDCU) instead
+// of a vector register, freeing register-file operand bandwidth.  `zero` is 0
+// but depends on a loop counter, so ptxas keeps the loads inside the loop
+// instead of hoisting the whole block into (spilled) registers.
+template <int K>
+struct alignas(16) DiskParam {
+    double2 c[DiskShape<K>::n_coef / 2];
+};
+template <int K, class T>
+struct ParamCoef {
+    const DiskParam<K>& P;
+    int zero;  // 0, but loop-variant: keeps the loads inside the step loop
+    template <int O>
+    __device__ __forceinline__ void get2(T& a, T& b) const {
+        const double2 v = P.c[zero + O / 2];
+        a = T(v.x);
+        b = T(v.y);
+    }
+};
+
+struct NoDiskParam {};
+
 template <int K, class T, int P>
 struct Powers {
     T pr[P][K + 1], pi[P][K + 1];  // P2[j]
