@@ -447,6 +447,10 @@ def run_ours(args):
                          "peak_source": "FP64 DFMA microbenchmark measured in this run (smc_fp64_peak, all SMs, "
                                         "8 chains/thread); MEASURED_PEAKS.json has no FP64 entry",
                          "flops_per_unit": F, "unit_of_work": "particle-step",
+                         "flops_note": "algorithmic flops = SURVEY.md 8(d) F_AD (the reference's 14 flops per "
+                                       "mode); the kernels execute fewer (4 DFMA per mode, Chebyshev "
+                                       "harmonics), so frac can exceed 1 — the FP64-pipe utilisation is "
+                                       "ncu's fp64_pipe_pct_active in profiles/r01_k1_<config>.md",
                          "traffic": _ncu_traffic(args.config)},
             "gpu_launches": launches,
             "clocks": clocks,
