@@ -22,8 +22,6 @@
 
 namespace smc::capi {
 
-constexpr int kLatticeTileHost = 8;  // == kLatticeTile (velocity.cuh) / kTileW (host_problem.cpp)
-
 extern thread_local std::string g_err;
 
 
