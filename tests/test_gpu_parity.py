@@ -448,3 +448,33 @@ def test_milstein_equals_euler_maruyama_for_isotropic_diffusion(ctx):
     em_b = S.observe_bvp(bvp, 606, ctx=ctx)
     bvp.scheme = S.StepScheme.milstein
     assert S.observe_bvp(bvp, 606, ctx=ctx) == em_b
+
+
+def test_concurrent_contexts_do_not_interfere():
+    """Two contexts (own streams and buffers) driven from two host threads at
+    once reproduce their serial results bit for bit — the kernel-parameter
+    coefficient path and every buffer are per launch / per context."""
+    import threading
+    u = [S.prior_draw(specs.C2_PRIOR, 808, 0xBE9C4, j, None) for j in range(2)]
+    spec = [specs.c2_spec(u[j], n_particles=20000) for j in range(2)]
+    for sp in spec:
+        sp.observations = sp.observations[:3]
+    ctxs = [S.Context(0), S.Context(0)]
+    serial = [S.observe_ad(spec[j], 808, ctx=ctxs[j]) for j in range(2)]
+    bvp = specs.paper_bvp(n_particles=2000)
+    serial_b = S.observe_bvp(bvp, 606, ctx=ctxs[1])
+    out = [None, None, None]
+
+    def run(j):
+        for _ in range(3):
+            out[j] = S.observe_ad(spec[j], 808, ctx=ctxs[j])
+            if j == 1:
+                out[2] = S.observe_bvp(bvp, 606, ctx=ctxs[1])
+    threads = [threading.Thread(target=run, args=(j,)) for j in range(2)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert out[0] == serial[0] and out[1] == serial[1] and out[2] == serial_b
+    for c in ctxs:
+        c.close()
