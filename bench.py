@@ -26,7 +26,9 @@ Printed on rank 0, one JSON line:
               sources) on this host's cores, bounded sample, rank 0 at N=1
 
 --impl reference runs the reference's own CPU implementation (oracle/_ref) of
-the same workload on all host cores instead.
+the same workload on all host cores instead.  --precision fp32 measures the
+optional FP32 variant of the kernels (roofline against an FFMA peak measured
+in the same run); the default and the headline are FP64.
 """
 from __future__ import annotations
 
@@ -294,7 +296,12 @@ def run_ours(args):
     S.load_library().smc_set_stream(ctx.handle, stream.cuda_stream)
 
     kind, payload, steps_per_eval, F, desc = build_workload(args.config, ctx)
-    peak = ctx.fp64_peak_tflops(300.0)
+    fp32 = args.precision == "fp32"
+    if fp32:  # the optional FP32 variant (north_star: within 3 SE of the FP64 result)
+        target = payload[0] if kind == "batched" else payload
+        target.precision = S.Precision.fp32
+        desc = dict(desc, workload=desc["workload"].replace("FP64", "FP32 variant"), precision="fp32")
+    peak = ctx.fp32_peak_tflops(300.0) if fp32 else ctx.fp64_peak_tflops(300.0)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
 
     def timed(fn):
@@ -436,22 +443,25 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "particle-steps/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
-            "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f32" if fp32 else "f64",
             "data": "synthetic (prior-draw velocity, reference recipe)",
             "config": dict(desc, parallelism=parallel, l2="flushed between steps (256 MiB write)"),
             "evals_per_sec": value / per_eval,
             "e2e": {"value": e2e_value, "unit": "particle-steps/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "evals_per_sec": e2e_value / per_eval, "api": api},
-            "roofline": {"bound": "fp64", "kernel": kernel_name, "achieved": achieved,
+            "roofline": {"bound": "fp32" if fp32 else "fp64", "kernel": kernel_name, "achieved": achieved,
                          "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                         "peak_source": "FP64 DFMA microbenchmark measured in this run (smc_fp64_peak, all SMs, "
-                                        "8 chains/thread); MEASURED_PEAKS.json has no FP64 entry",
+                         "peak_source": ("FP32 FFMA microbenchmark measured in this run (smc_fp32_peak, all SMs, "
+                                         "8 chains/thread); MEASURED_PEAKS.json has no FP32 entry" if fp32 else
+                                         "FP64 DFMA microbenchmark measured in this run (smc_fp64_peak, all SMs, "
+                                         "8 chains/thread); MEASURED_PEAKS.json has no FP64 entry"),
                          "flops_per_unit": F, "unit_of_work": "particle-step",
                          "flops_note": "algorithmic flops = SURVEY.md 8(d) F_AD (the reference's 14 flops per "
-                                       "mode); the kernels execute fewer (4 DFMA per mode, Chebyshev "
-                                       "harmonics), so frac can exceed 1 — the FP64-pipe utilisation is "
-                                       "ncu's fp64_pipe_pct_active in profiles/r01_k1_<config>.md",
-                         "traffic": _ncu_traffic(args.config)},
+                                       "mode); the kernels execute fewer (4 FMA per mode, Chebyshev "
+                                       "harmonics), so frac can exceed 1 — the pipe utilisation is ncu's "
+                                       + ("fma_pipe_pct_active in profiles/r01_k1_<config>_fp32.md" if fp32 else
+                                          "fp64_pipe_pct_active in profiles/r01_k1_<config>.md"),
+                         "traffic": _ncu_traffic(args.config + ("_fp32" if fp32 else ""))},
             "gpu_launches": launches,
             "clocks": clocks,
         }
@@ -536,6 +546,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
+                    help="fp32 = the optional FP32 variant of the kernels (our arm only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: test the multi-rank path with fewer GPUs than ranks")

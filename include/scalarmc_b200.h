@@ -365,6 +365,9 @@ smc_status smc_last_stats(smc_ctx* ctx, smc_stats* out);
 /* FP64 DFMA peak microbenchmark (roofline denominator): runs a DFMA-only
  * kernel over all SMs for about `ms` milliseconds; returns TFLOP/s. */
 smc_status smc_fp64_peak(smc_ctx* ctx, double ms, double* tflops);
+/* The FP32 counterpart (FFMA-only kernel): the roofline denominator of the
+ * SMC_FP32 variant. */
+smc_status smc_fp32_peak(smc_ctx* ctx, double ms, double* tflops);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

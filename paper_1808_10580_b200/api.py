@@ -487,6 +487,11 @@ class Context:
         _check(self.lib.smc_fp64_peak(self.handle, ms, C.byref(out)))
         return out.value
 
+    def fp32_peak_tflops(self, ms: float = 200.0) -> float:
+        out = C.c_double()
+        _check(self.lib.smc_fp32_peak(self.handle, ms, C.byref(out)))
+        return out.value
+
 
 _contexts: dict[int, Context] = {}
 

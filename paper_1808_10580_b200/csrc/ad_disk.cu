@@ -14,6 +14,7 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <utility>
 
 #include "ad_body.cuh"
@@ -56,8 +57,20 @@ __global__ void __launch_bounds__(kBlock, MINB) ad_particles_disk(const AdLaunch
 // value that is 0 but varies with the step counter, so ptxas keeps them
 // inside the loop instead of hoisting ~200 coefficients into spilled
 // registers.
+// FP64: DiskParam<K, double> read through ParamCoef; FP32: the packed
+// FFMA2 block (PackedParam, disk_velocity.cuh).
+template <int K, class T>
+struct ParamBlock {
+    using type = DiskParam<K, double>;
+};
+template <int K>
+struct ParamBlock<K, float> {
+    using type = PackedParam<K>;
+};
+
 template <int K, class T, int MINB>
-__global__ void __launch_bounds__(kBlock, MINB) ad_particles_disk_param(const AdLaunch L, const DiskParam<K> P) {
+__global__ void __launch_bounds__(kBlock, MINB)
+    ad_particles_disk_param(const AdLaunch L, const typename ParamBlock<K, T>::type P) {
     const int obs = blockIdx.y;
     const int64_t span = L.p_end - L.p_begin;
     const int64_t base = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x;
@@ -65,16 +78,35 @@ __global__ void __launch_bounds__(kBlock, MINB) ad_particles_disk_param(const Ad
     int64_t local[1] = {base};
     ad_particles_p<T, 1>(L, obs, 0, local, span,
                          [&](const T (&x1)[1], const T (&x2)[1], T (&v1)[1], T (&v2)[1], int zero) {
-                             const ParamCoef<K, T> C{P, zero};
-                             velocity_disk<K, T, 1>(C, x1, x2, v1, v2);
+                             if constexpr (std::is_same<T, float>::value) {
+                                 const PackedCoef<K> C{P};
+                                 velocity_disk<K, T, 1>(C, x1, x2, v1, v2);
+                             } else {
+                                 const ParamCoef<K, T> C{P, zero};
+                                 velocity_disk<K, T, 1>(C, x1, x2, v1, v2);
+                             }
                          });
 }
 
 template <int K, class T>
 cudaError_t launch_param(const AdLaunch& L, cudaStream_t s) {
     static_assert(DiskShape<K>::n_coef % 2 == 0, "coefficient pairs");
-    DiskParam<K> P;
-    std::memcpy(&P, L.host_disk, sizeof(P));
+    typename ParamBlock<K, T>::type P;
+    if constexpr (std::is_same<T, double>::value) {
+        std::memcpy(&P, L.host_disk, sizeof(P));
+    } else {  // float conversion as the shared-memory staging does it; pairs expanded for FFMA2
+        const double* h = L.host_disk;
+        float* dst = P.c;
+        for (int i = 0; i < DiskShape<K>::n_pairs; ++i) {
+            const float ar = float(h[4 * i]), ai = float(h[4 * i + 1]), br = float(h[4 * i + 2]),
+                        bi = float(h[4 * i + 3]);
+            const float e[8] = {ar, ai, br, bi, -bi, br, -ai, ar};
+            for (int q = 0; q < 8; ++q) dst[8 * i + q] = e[q];
+        }
+        for (int i = DiskShape<K>::row0_offset; i < DiskShape<K>::n_coef; ++i)
+            dst[i + PackedShape<K>::shift] = float(h[i]);
+        for (int i = PackedShape<K>::n_coef; i < PackedShape<K>::n_padded; ++i) dst[i] = 0.0f;
+    }
     const int64_t span = L.p_end - L.p_begin;
     const dim3 grid(static_cast<unsigned>((span + kBlock - 1) / kBlock), static_cast<unsigned>(L.n_obs), 1);
     ad_particles_disk_param<K, T, (K <= 8 ? 4 : 3)><<<grid, kBlock, 0, s>>>(L, P);
@@ -82,7 +114,7 @@ cudaError_t launch_param(const AdLaunch& L, cudaStream_t s) {
 }
 
 template <class T>
-cudaError_t dispatch_param(const AdLaunch& L, int K, cudaStream_t s) {  // T = double
+cudaError_t dispatch_param(const AdLaunch& L, int K, cudaStream_t s) {
     switch (K) {
         case 1: return launch_param<1, T>(L, s);
         case 2: return launch_param<2, T>(L, s);
@@ -154,9 +186,8 @@ cudaError_t launch_ad_disk(const AdLaunch& L, int K, const double* coef, cudaStr
     // one coefficient block with its host copy: the kernel-parameter path
     // (SMC_DISK_P=2 keeps the shared-memory kernel, which has the P=2 form)
     const char* pe = std::getenv("SMC_DISK_P");
-    // (FP64 only: FP32 would convert every coefficient on every use)
-    if (L.n_samples == 1 && L.host_disk && L.precision != 1 && !(pe && std::atoi(pe) == 2))
-        return dispatch_param<double>(L, K, s);
+    if (L.n_samples == 1 && L.host_disk && !(pe && std::atoi(pe) == 2))
+        return L.precision == 1 ? dispatch_param<float>(L, K, s) : dispatch_param<double>(L, K, s);
     return L.precision == 1 ? dispatch<float>(L, K, coef, s) : dispatch<double>(L, K, coef, s);
 }
 

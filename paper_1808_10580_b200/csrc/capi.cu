@@ -576,28 +576,37 @@ smc_status smc_last_stats(smc_ctx* ctx, smc_stats* out) {
     });
 }
 
+namespace {
+// Runs the DFMA (fp64) or FFMA peak kernel over all SMs for about `ms`.
+double fma_peak(smc_ctx* ctx, double ms, bool fp64) {
+    CK(cudaSetDevice(ctx->device));
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    const int blocks = sms * 8;
+    double* sink = ctx->tmp_a.get<double>(static_cast<size_t>(blocks));
+    int iters = 4096;
+    float t = 0.f;
+    for (int attempt = 0; attempt < 8; ++attempt) {
+        CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+        CK(fp64 ? launch_dfma_peak(blocks, iters, sink, ctx->stream) : launch_ffma_peak(blocks, iters, sink, ctx->stream));
+        CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+        CK(cudaEventSynchronize(ctx->ev[1]));
+        CK(cudaEventElapsedTime(&t, ctx->ev[0], ctx->ev[1]));
+        if (t >= 0.9 * ms) break;
+        const double scale = std::min(64.0, std::max(2.0, ms / std::max<double>(t, 1e-3)));
+        iters = static_cast<int>(std::min<double>(iters * scale, 1 << 30));
+    }
+    const double flops = 2.0 * 8.0 * double(iters) * 256.0 * blocks;
+    return flops / (double(t) * 1e-3) / 1e12;
+}
+}  // namespace
+
+smc_status smc_fp32_peak(smc_ctx* ctx, double ms, double* tflops) {
+    return guarded([&] { *tflops = fma_peak(ctx, ms, false); });
+}
+
 smc_status smc_fp64_peak(smc_ctx* ctx, double ms, double* tflops) {
-    return guarded([&] {
-        CK(cudaSetDevice(ctx->device));
-        int sms = 0;
-        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
-        const int blocks = sms * 8;
-        double* sink = ctx->tmp_a.get<double>(static_cast<size_t>(blocks));
-        int iters = 4096;
-        float t = 0.f;
-        for (int attempt = 0; attempt < 8; ++attempt) {
-            CK(cudaEventRecord(ctx->ev[0], ctx->stream));
-            CK(launch_dfma_peak(blocks, iters, sink, ctx->stream));
-            CK(cudaEventRecord(ctx->ev[1], ctx->stream));
-            CK(cudaEventSynchronize(ctx->ev[1]));
-            CK(cudaEventElapsedTime(&t, ctx->ev[0], ctx->ev[1]));
-            if (t >= 0.9 * ms) break;
-            const double scale = std::min(64.0, std::max(2.0, ms / std::max<double>(t, 1e-3)));
-            iters = static_cast<int>(std::min<double>(iters * scale, 1 << 30));
-        }
-        const double flops = 2.0 * 8.0 * double(iters) * 256.0 * blocks;
-        *tflops = flops / (double(t) * 1e-3) / 1e12;
-    });
+    return guarded([&] { *tflops = fma_peak(ctx, ms, true); });
 }
 
 smc_status smc_bvp_observe(smc_ctx* ctx, const smc_bvp_problem* p, uint64_t seed, smc_estimate* out) {

@@ -38,27 +38,124 @@ template <int O>
 __device__ __forceinline__ void SmemCoef<float>::get2(float& a, float& b) const {
     asm volatile("ld.shared.v2.f32 {%0, %1}, [%2+%3];" : "=f"(a), "=f"(b) : "r"(base), "n"(O * 4));
 }
+// Four consecutive coefficients (O a multiple of 4): one 16-byte load for
+// FP32, two for FP64.
+template <int O, class T, class CA>
+__device__ __forceinline__ void get4(const CA& C, T& a, T& b, T& c, T& d) {
+    C.template get2<O>(a, b);
+    C.template get2<O + 2>(c, d);
+}
+template <int O>
+__device__ __forceinline__ void get4(const SmemCoef<float>& C, float& a, float& b, float& c, float& d) {
+    static_assert(O % 4 == 0, "16-byte aligned");
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4+%5];"
+                 : "=f"(a), "=f"(b), "=f"(c), "=f"(d)
+                 : "r"(C.base), "n"(O * 4));
+}
 
 // Coefficient block passed BY VALUE as a kernel parameter (constant bank 0):
 // the DFMAs then take each coefficient from a uniform register (LDCU) instead
 // of a vector register, freeing register-file operand bandwidth.  `zero` is 0
 // but depends on a loop counter, so ptxas keeps the loads inside the loop
 // instead of hoisting the whole block into (spilled) registers.
-template <int K>
+// The block is stored in the compute type (FP32 launches convert it once on
+// the host, exactly as the shared-memory staging does on the device).
+template <class T>
+struct Vec2Of;
+template <>
+struct Vec2Of<double> {
+    using type = double2;
+};
+template <>
+struct Vec2Of<float> {
+    using type = float2;
+};
+template <int K, class T = double>
 struct alignas(16) DiskParam {
-    double2 c[DiskShape<K>::n_coef / 2];
+    typename Vec2Of<T>::type c[DiskShape<K>::n_coef / 2];
 };
 template <int K, class T>
 struct ParamCoef {
-    const DiskParam<K>& P;
+    const DiskParam<K, T>& P;
     int zero;  // 0, but loop-variant: keeps the loads inside the step loop
+    // FP64 indexes by `zero` (LDCU.64 from a uniform-register address); FP32
+    // uses immediate offsets, which ptxas turns into LDCU.128 (four
+    // coefficients per issue slot — the FP32 kernel is issue-bound) and can
+    // afford: hoisting part of the float block spills nothing, while the
+    // double block spills at every K >= 4.
     template <int O>
     __device__ __forceinline__ void get2(T& a, T& b) const {
-        const double2 v = P.c[zero + O / 2];
-        a = T(v.x);
-        b = T(v.y);
+        const auto v = P.c[(std::is_same<T, double>::value ? zero : 0) + O / 2];
+        a = v.x;
+        b = v.y;
     }
 };
+
+template <int O, int K>
+__device__ __forceinline__ void get4(const ParamCoef<K, float>& C, float& a, float& b, float& c, float& d) {
+    static_assert(O % 4 == 0, "16-byte aligned");
+    const float4 v = reinterpret_cast<const float4*>(C.P.c)[O / 4];
+    a = v.x;
+    b = v.y;
+    c = v.z;
+    d = v.w;
+}
+
+// FP32 packed form (FFMA2, sm_100a's fma.rn.f32x2): the pair update is four
+// two-lane FMAs, (Ar, Ai) += (ar, ai) pr + (-bi, br) pi and
+// (Br, Bi) += (br, bi) qr + (-ai, ar) qi, each taking a coefficient pair
+// from a uniform register and the power as a broadcast scalar.  Per lane
+// it is the same FMA sequence as the scalar form (identical results) in
+// half the issue slots; the FP32 kernel is issue-bound, FFMA2 runs at the
+// FFMA flop rate (tools/ubench_ffma2.cu).  The block stores each pair as
+// (ar, ai, br, bi, -bi, br, -ai, ar); row0 and g0 follow as in disk_shape.h.
+template <int K>
+struct PackedShape {
+    static constexpr int n_pairs = DiskShape<K>::n_pairs;
+    static constexpr int shift = 4 * n_pairs;  // extra floats before row0
+    static constexpr int n_coef = DiskShape<K>::n_coef + shift;
+    static constexpr int n_padded = (n_coef + 3) / 4 * 4;
+};
+template <int K>
+struct alignas(16) PackedParam {
+    float c[PackedShape<K>::n_padded];
+};
+template <int K>
+struct PackedCoef {
+    const PackedParam<K>& P;
+    template <int O>  // O: offset in the disk_shape.h layout (row0 / g0 only)
+    __device__ __forceinline__ void get2(float& a, float& b) const {
+        static_assert(O >= DiskShape<K>::row0_offset, "pairs use pair4");
+        a = P.c[O + PackedShape<K>::shift];
+        b = P.c[O + PackedShape<K>::shift + 1];
+    }
+    template <int I>  // the I-th pair's four coefficient pairs
+    __device__ __forceinline__ void pair4(uint64_t& c0, uint64_t& c1, uint64_t& c2, uint64_t& c3) const {
+        const ulonglong2* q = reinterpret_cast<const ulonglong2*>(P.c) + 2 * I;
+        const ulonglong2 u = q[0], v = q[1];
+        c0 = u.x;
+        c1 = u.y;
+        c2 = v.x;
+        c3 = v.y;
+    }
+};
+template <class CA>
+struct IsPacked : std::false_type {};
+template <int K>
+struct IsPacked<PackedCoef<K>> : std::true_type {};
+
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t v, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+// acc += c * (s, s)   (ptxas folds the broadcast into the FFMA2 operand)
+__device__ __forceinline__ void f2_fma_bcast(uint64_t& acc, uint64_t c, float s) {
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(c), "l"(f2_pack(s, s)));
+}
 
 struct NoDiskParam {};
 
@@ -80,8 +177,7 @@ template <int K, int K1, int J, class T, int P, class CA>
 __device__ __forceinline__ void disk_pair(const CA& C, const Powers<K, T, P>& W, RowAcc<P, T>& a) {
     constexpr int o = 4 * (DiskShape<K>::pair_offset(K1) + J - 1);
     T ar, ai, br, bi;
-    C.template get2<o>(ar, ai);
-    C.template get2<o + 2>(br, bi);
+    get4<o>(C, ar, ai, br, bi);
 #pragma unroll
     for (int p = 0; p < P; ++p) {
         a.Ar[p] = fma(ar, W.pr[p][J], a.Ar[p]);
@@ -95,19 +191,37 @@ __device__ __forceinline__ void disk_pair(const CA& C, const Powers<K, T, P>& W,
     }
 }
 
+template <int K, int K1, int J, class W_t>
+__device__ __forceinline__ void disk_pair_packed(const PackedCoef<K>& C, const W_t& W, uint64_t& A, uint64_t& B) {
+    uint64_t c0, c1, c2, c3;
+    C.template pair4<DiskShape<K>::pair_offset(K1) + J - 1>(c0, c1, c2, c3);
+    f2_fma_bcast(A, c0, W.pr[0][J]);
+    f2_fma_bcast(B, c1, W.qr[0][J]);
+    f2_fma_bcast(A, c2, W.pi[0][J]);
+    f2_fma_bcast(B, c3, W.qi[0][J]);
+}
+
+template <int K, int K1, class W_t, int... Js>
+__device__ __forceinline__ void disk_row_pairs_packed(const PackedCoef<K>& C, const W_t& W, uint64_t& A, uint64_t& B,
+                                                      std::integer_sequence<int, Js...>) {
+    (disk_pair_packed<K, K1, Js + 1>(C, W, A, B), ...);
+}
+
 template <int K, int K1, class T, int P, class CA, int... Js>
 __device__ __forceinline__ void disk_row_pairs(const CA& C, const Powers<K, T, P>& W, RowAcc<P, T>& a,
                                                std::integer_sequence<int, Js...>) {
     (disk_pair<K, K1, Js + 1, T, P>(C, W, a), ...);
 }
 
-// Harmonics e^{i k theta} for k = 2..K.  FP64: the Chebyshev recurrence
-// X_k = 2 cos(theta) X_{k-1} - X_{k-2} (2 DFMA per k instead of the 4 of a
-// complex multiply; rounding error grows like eps k^2 — 1e-14 at k = 12,
-// 1e-12 at k = 80, far inside the 1e-10 parity gate).  FP32 keeps the complex
-// product (eps k^2 would be 4e-4 at k = 80).
+// Harmonics e^{i k theta} for k = 2..K: the Chebyshev recurrence
+// X_k = 2 cos(theta) X_{k-1} - X_{k-2} (2 FMA per k instead of the 4 of a
+// complex multiply).  Its rounding error grows like eps k^2: FP64 1e-14 at
+// the disk kernels' K <= 12, far inside the 1e-10 parity gate; FP32 ~1e-5,
+// two orders below the Monte Carlo standard error of any launch large enough
+// to be worth the FP32 variant (the gate there is 3 SE).  The tiled generic
+// kernel (K up to 80, where FP32 would reach 4e-4) keeps complex products.
 template <class T>
-constexpr bool kChebyshev = std::is_same<T, double>::value;
+constexpr bool kChebyshev = true;
 
 // Row k1 >= 1: P1 <- P1 e1 (k1 > 1), row sums A and B', then
 //   v2 += k1 Re(P1 A),  v1 -= Re(P1 B').  (q1r, q1i) = P1[k1 - 1] for the
@@ -137,14 +251,22 @@ __device__ __forceinline__ void disk_row(const CA& C, const Powers<K, T, P>& W, 
     T g0r, g0i;
     C.template get2<S::g0_offset + 2 * (K1 - 1)>(g0r, g0i);
     RowAcc<P, T> a;
+    if constexpr (IsPacked<CA>::value) {
+        static_assert(P == 1 && std::is_same<T, float>::value, "packed form: FP32, one particle per thread");
+        uint64_t A = f2_pack(g0r, g0i), B = f2_pack(0.0f, 0.0f);
+        disk_row_pairs_packed<K, K1>(C, W, A, B, std::make_integer_sequence<int, S::jmax(K1)>{});
+        f2_unpack(A, a.Ar[0], a.Ai[0]);
+        f2_unpack(B, a.Br[0], a.Bi[0]);
+    } else {
 #pragma unroll
-    for (int p = 0; p < P; ++p) {
-        a.Ar[p] = g0r;
-        a.Ai[p] = g0i;
-        a.Br[p] = T(0);
-        a.Bi[p] = T(0);
+        for (int p = 0; p < P; ++p) {
+            a.Ar[p] = g0r;
+            a.Ai[p] = g0i;
+            a.Br[p] = T(0);
+            a.Bi[p] = T(0);
+        }
+        disk_row_pairs<K, K1, T, P>(C, W, a, std::make_integer_sequence<int, S::jmax(K1)>{});
     }
-    disk_row_pairs<K, K1, T, P>(C, W, a, std::make_integer_sequence<int, S::jmax(K1)>{});
 #pragma unroll
     for (int p = 0; p < P; ++p) {
         acc2[p] = fma(T(K1), fma(p1r[p], a.Ar[p], -p1i[p] * a.Ai[p]), acc2[p]);

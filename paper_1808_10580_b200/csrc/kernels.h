@@ -179,5 +179,6 @@ cudaError_t launch_philox(int64_t n, const uint32_t* ctr, const uint32_t* key, u
 cudaError_t launch_normal_pairs(uint64_t seed, uint32_t obs, uint32_t particle, int64_t n,
                                 double* out, cudaStream_t s);
 cudaError_t launch_dfma_peak(int n_blocks, int iters, double* sink, cudaStream_t s);
+cudaError_t launch_ffma_peak(int n_blocks, int iters, double* sink, cudaStream_t s);
 
 }  // namespace smc

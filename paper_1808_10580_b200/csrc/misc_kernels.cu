@@ -49,6 +49,22 @@ __global__ void __launch_bounds__(256) dfma_peak_kernel(int iters, double* sink)
     if (s == 12345.0) sink[blockIdx.x] = s;  // never true; keeps the chains live
 }
 
+// The FP32 counterpart: 8 independent FFMA chains per thread.
+__global__ void __launch_bounds__(256) ffma_peak_kernel(int iters, double* sink) {
+    float a[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a[q] = 1.0f + 1e-6f * float(threadIdx.x + q);
+    const float b = 0.9999999f, c = 1e-9f;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) a[q] = fmaf(a[q], b, c);
+    }
+    float s = 0.0f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += a[q];
+    if (s == 12345.0f) sink[blockIdx.x] = s;  // never true; keeps the chains live
+}
+
 }  // namespace
 
 cudaError_t launch_philox(int64_t n, const uint32_t* ctr, const uint32_t* key, uint32_t* out, cudaStream_t s) {
@@ -64,6 +80,11 @@ cudaError_t launch_normal_pairs(uint64_t seed, uint32_t obs, uint32_t particle, 
 
 cudaError_t launch_dfma_peak(int n_blocks, int iters, double* sink, cudaStream_t s) {
     dfma_peak_kernel<<<n_blocks, 256, 0, s>>>(iters, sink);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ffma_peak(int n_blocks, int iters, double* sink, cudaStream_t s) {
+    ffma_peak_kernel<<<n_blocks, 256, 0, s>>>(iters, sink);
     return cudaGetLastError();
 }
 

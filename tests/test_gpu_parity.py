@@ -285,6 +285,20 @@ def test_fp32_within_three_standard_errors(ctx, golden):
         assert abs(e.mean - r["mean"]) <= 3.0 * r["std_error"]
 
 
+def test_fp32_param_path_matches_shared_memory_path(ctx, golden, monkeypatch):
+    """FP32 single-sample launches take the coefficient block as a kernel
+    parameter (converted to float on the host); the shared-memory kernel
+    (SMC_DISK_P=2) converts on the device.  Same floats, same arithmetic per
+    particle: identical particle values."""
+    u = unhex(golden["c2"]["u"])
+    spec = specs.c2_spec(u, n_particles=4096, precision=S.Precision.fp32)
+    a = [S.ad_particle_values(spec, j, 808, 4096, ctx) for j in (0, 8)]
+    monkeypatch.setenv("SMC_DISK_P", "2")
+    b = [S.ad_particle_values(spec, j, 808, 4096, ctx) for j in (0, 8)]
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y), float(np.max(np.abs(x - y)))
+
+
 # ---------------------------------------------------------------- BVP ------
 def test_bvp_box_matches_reference(ctx, golden):
     g = golden["bvp_box"]
