@@ -20,8 +20,10 @@ __device__ __forceinline__ double log_t(double x) { return fm::log_tab(x); }  //
 __device__ __forceinline__ float log_t(float x) { return __logf(x); }
 
 // Particles local[p] (p < P) of observation `obs`; entries >= span are
-// computed on a clamped index and not stored.
-template <class T, int P, class Vel>
+// computed on a clamped index and not stored.  RK: the launch carries the
+// Philox round keys of L.seed (L.rk; single-sample launches without per-sample
+// seeds).
+template <class T, int P, class Vel, bool RK = false>
 __device__ __forceinline__ void ad_particles_p(const AdLaunch& L, int obs, int sample, const int64_t (&local)[P],
                                                int64_t span, Vel&& velocity) {
     const AdObsImg o = L.obs[obs];
@@ -46,7 +48,8 @@ __device__ __forceinline__ void ad_particles_p(const AdLaunch& L, int obs, int s
     auto draw = [&](int64_t step, T (&z1)[P], T (&z2)[P]) {
 #pragma unroll
         for (int p = 0; p < P; ++p) {
-            const Uniform2 u = uniform_block(k0, k1, slot, particle[p], static_cast<uint64_t>(step));
+            const Uniform2 u = RK ? uniform_block(L.rk, slot, particle[p], static_cast<uint64_t>(step))
+                                  : uniform_block(k0, k1, slot, particle[p], static_cast<uint64_t>(step));
             const T rad = sqrt(T(-2) * log_t(T(u.u0)));
             T sn, cs;
             sincospi_t(T(2) * T(u.u1), &sn, &cs);

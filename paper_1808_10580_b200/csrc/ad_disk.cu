@@ -76,8 +76,7 @@ __global__ void __launch_bounds__(kBlock, MINB)
     const int64_t base = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x;
     if (base >= span) return;
     int64_t local[1] = {base};
-    ad_particles_p<T, 1>(L, obs, 0, local, span,
-                         [&](const T (&x1)[1], const T (&x2)[1], T (&v1)[1], T (&v2)[1], int zero) {
+    auto vel = [&](const T (&x1)[1], const T (&x2)[1], T (&v1)[1], T (&v2)[1], int zero) {
                              if constexpr (std::is_same<T, float>::value) {
                                  const PackedCoef<K> C{P};
                                  velocity_disk<K, T, 1>(C, x1, x2, v1, v2);
@@ -85,7 +84,12 @@ __global__ void __launch_bounds__(kBlock, MINB)
                                  const ParamCoef<K, T> C{P, zero};
                                  velocity_disk<K, T, 1>(C, x1, x2, v1, v2);
                              }
-                         });
+                         };
+    // FP32 takes the Philox round keys from the parameter bank too; FP64 does
+    // not: the keys then occupy uniform registers that the step counter needs,
+    // `zero` moves to a vector register and every coefficient load becomes a
+    // per-thread LDC (C2 31.7 -> 43.2 ms measured)
+    ad_particles_p<T, 1, decltype(vel)&, std::is_same<T, float>::value>(L, obs, 0, local, span, vel);
 }
 
 template <int K, class T>
@@ -109,7 +113,9 @@ cudaError_t launch_param(const AdLaunch& L, cudaStream_t s) {
     }
     const int64_t span = L.p_end - L.p_begin;
     const dim3 grid(static_cast<unsigned>((span + kBlock - 1) / kBlock), static_cast<unsigned>(L.n_obs), 1);
-    ad_particles_disk_param<K, T, (K <= 8 ? 4 : 3)><<<grid, kBlock, 0, s>>>(L, P);
+    AdLaunch LK = L;
+    LK.rk = make_round_keys(L.seed);
+    ad_particles_disk_param<K, T, (K <= 8 ? 4 : 3)><<<grid, kBlock, 0, s>>>(LK, P);
     return cudaGetLastError();
 }
 
@@ -186,7 +192,7 @@ cudaError_t launch_ad_disk(const AdLaunch& L, int K, const double* coef, cudaStr
     // one coefficient block with its host copy: the kernel-parameter path
     // (SMC_DISK_P=2 keeps the shared-memory kernel, which has the P=2 form)
     const char* pe = std::getenv("SMC_DISK_P");
-    if (L.n_samples == 1 && L.host_disk && !(pe && std::atoi(pe) == 2))
+    if (L.n_samples == 1 && L.host_disk && !L.seeds && !(pe && std::atoi(pe) == 2))
         return L.precision == 1 ? dispatch_param<float>(L, K, s) : dispatch_param<double>(L, K, s);
     return L.precision == 1 ? dispatch<float>(L, K, coef, s) : dispatch<double>(L, K, coef, s);
 }

@@ -100,7 +100,6 @@ __global__ void __launch_bounds__(kBvpBlock) bvp_walkers(const BvpLaunch L) {
     const disk::SmemCoef<T> dc{static_cast<uint32_t>(__cvta_generic_to_shared(disk_coef))};
     const int lane = threadIdx.x & 31;
     const unsigned long long total = static_cast<unsigned long long>(L.n_obs) * L.n_particles;
-    const uint32_t k0 = static_cast<uint32_t>(L.seed), k1 = static_cast<uint32_t>(L.seed >> 32);
     const LatticeImg& lat = L.vel.lat;
     const T dt = T(L.dt), sr = T(L.sr);
 
@@ -144,7 +143,7 @@ __global__ void __launch_bounds__(kBvpBlock) bvp_walkers(const BvpLaunch L) {
         }
         if (!__any_sync(FULL, active)) break;
         if (active) {
-            const Uniform2 u = uniform_block(k0, k1, L.obs_slot0 + obs, particle, static_cast<uint64_t>(step));
+            const Uniform2 u = uniform_block(L.rk, L.obs_slot0 + obs, particle, static_cast<uint64_t>(step));
             T xi1, xi2, v1, v2;
             if constexpr (STRICT) {
                 const double r = sqrt(-2.0 * log(u.u0));

@@ -11,7 +11,8 @@
 
 namespace smc {
 
-cudaError_t launch_bvp_disk(const BvpLaunch& L, unsigned blocks, cudaStream_t s) {
+cudaError_t launch_bvp_disk(const BvpLaunch& L0, unsigned blocks, cudaStream_t s) {
+    const BvpLaunch L = with_round_keys(L0);
     switch (L.disk_K) {
 #define SMC_BVP_DISK_CASE(K) \
     case K: bvp_walkers<double, false, 0, 0, 0, false, K><<<blocks, kBvpBlock, 0, s>>>(L); break;

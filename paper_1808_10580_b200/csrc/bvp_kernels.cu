@@ -35,7 +35,8 @@ unsigned blocks_per_sm() {
 
 }  // namespace
 
-cudaError_t launch_bvp_walkers(const BvpLaunch& L, int n_sms, cudaStream_t s) {
+cudaError_t launch_bvp_walkers(const BvpLaunch& L0, int n_sms, cudaStream_t s) {
+    const BvpLaunch L = with_round_keys(L0);
     // Persistent grid: enough resident warps to hide latency on every SM.
     const unsigned long long total = static_cast<unsigned long long>(L.n_obs) * L.n_particles;
     unsigned blocks = static_cast<unsigned>(n_sms) * blocks_per_sm();
@@ -51,7 +52,8 @@ cudaError_t launch_bvp_walkers(const BvpLaunch& L, int n_sms, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_bvp_basis(const BvpLaunch& L, int n_sms, cudaStream_t s) {
+cudaError_t launch_bvp_basis(const BvpLaunch& L0, int n_sms, cudaStream_t s) {
+    const BvpLaunch L = with_round_keys(L0);
     const unsigned long long total = static_cast<unsigned long long>(L.n_obs) * L.n_particles;
     unsigned blocks = static_cast<unsigned>(n_sms) * blocks_per_sm();
     const unsigned long long need = (total + kBvpBlock - 1) / kBvpBlock;

@@ -9,7 +9,8 @@
 
 namespace smc {
 
-cudaError_t launch_bvp_walkers_strict(const BvpLaunch& L, int n_sms, cudaStream_t s) {
+cudaError_t launch_bvp_walkers_strict(const BvpLaunch& L0, int n_sms, cudaStream_t s) {
+    const BvpLaunch L = with_round_keys(L0);
     const unsigned long long total = static_cast<unsigned long long>(L.n_obs) * L.n_particles;
     unsigned blocks = static_cast<unsigned>(n_sms) * 8u;
     const unsigned long long need = (total + kBvpBlock - 1) / kBvpBlock;

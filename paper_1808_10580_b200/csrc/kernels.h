@@ -8,6 +8,7 @@
 
 #include "geometry.cuh"
 #include "images.h"
+#include "smc_device.cuh"
 
 namespace smc {
 
@@ -32,6 +33,7 @@ struct AdLaunch {
     double sigma;              // sqrt(2 kappa)
     double* values;            // [n_samples][n_obs][p_end - p_begin]
     const double* host_disk;   // host copy of the single-sample disk coefficient block (or null)
+    RoundKeys rk;              // Philox round keys of `seed` (filled by the launcher that uses them)
 };
 
 cudaError_t launch_ad_particles(const AdLaunch& L, cudaStream_t s);
@@ -69,7 +71,14 @@ struct BvpLaunch {
     const double* disk_coef;   // disk_shape.h coefficient block when disk_K > 0
     int32_t disk_K;            // > 0: dense Fourier velocity on |k| <= disk_K (FP64 walkers use bvp_disk.cu)
     int32_t pad2_;
+    RoundKeys rk;              // Philox round keys of `seed` (with_round_keys, set by every K2 launcher)
 };
+
+inline BvpLaunch with_round_keys(const BvpLaunch& L) {
+    BvpLaunch K = L;
+    K.rk = make_round_keys(L.seed);
+    return K;
+}
 
 cudaError_t launch_bvp_walkers(const BvpLaunch& L, int n_sms, cudaStream_t s);
 cudaError_t launch_bvp_walkers_strict(const BvpLaunch& L, int n_sms, cudaStream_t s);

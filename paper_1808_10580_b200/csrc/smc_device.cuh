@@ -40,6 +40,37 @@ SMC_HD u32x4 philox4x32_10(u32x4 c, uint32_t k0, uint32_t k1) {
     return c;
 }
 
+// The same block with the 20 round keys precomputed on the host
+// (k0 + r W0, k1 + r W1 for r = 0..9, mod 2^32 — identical words): when the
+// keys sit in the kernel's parameter bank the XORs take them as uniform
+// operands, instead of re-deriving the key schedule every step (20 uniform
+// adds per block; the walker kernel is issue-bound).
+struct RoundKeys {
+    uint32_t k[20];
+};
+inline RoundKeys make_round_keys(uint64_t seed) {
+    RoundKeys r;
+    uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
+    for (int round = 0; round < 10; ++round) {
+        r.k[2 * round] = k0;
+        r.k[2 * round + 1] = k1;
+        k0 += kPhiloxW0;
+        k1 += kPhiloxW1;
+    }
+    return r;
+}
+SMC_HD u32x4 philox4x32_10(u32x4 c, const RoundKeys& rk) {
+#pragma unroll
+    for (int round = 0; round < 10; ++round) {
+        const uint64_t p0 = static_cast<uint64_t>(kPhiloxM0) * c.x;
+        const uint64_t p1 = static_cast<uint64_t>(kPhiloxM1) * c.z;
+        const uint32_t hi0 = static_cast<uint32_t>(p0 >> 32), lo0 = static_cast<uint32_t>(p0);
+        const uint32_t hi1 = static_cast<uint32_t>(p1 >> 32), lo1 = static_cast<uint32_t>(p1);
+        c = u32x4{hi1 ^ c.y ^ rk.k[2 * round], lo1, hi0 ^ c.w ^ rk.k[2 * round + 1], lo0};
+    }
+    return c;
+}
+
 // 53 random bits into (0,1): ((m) + 0.5) * 2^-53 with IEEE rounding of the
 // add — bit-identical to rng.cpp:59-64.  m < 2^53, so the conversion is exact.
 SMC_HD double u53_to_unit(uint64_t word) {
@@ -62,6 +93,14 @@ SMC_HD Uniform2 uniform_block(uint32_t k0, uint32_t k1, uint32_t obs, uint32_t p
                               uint64_t step) {
     const u32x4 r = philox4x32_10(
         u32x4{static_cast<uint32_t>(step), static_cast<uint32_t>(step >> 32), obs, particle}, k0, k1);
+    const uint64_t a = (static_cast<uint64_t>(r.y) << 32) | r.x;
+    const uint64_t b = (static_cast<uint64_t>(r.w) << 32) | r.z;
+    return Uniform2{u53_to_unit(a), u53_to_unit(b)};
+}
+
+SMC_HD Uniform2 uniform_block(const RoundKeys& rk, uint32_t obs, uint32_t particle, uint64_t step) {
+    const u32x4 r = philox4x32_10(
+        u32x4{static_cast<uint32_t>(step), static_cast<uint32_t>(step >> 32), obs, particle}, rk);
     const uint64_t a = (static_cast<uint64_t>(r.y) << 32) | r.x;
     const uint64_t b = (static_cast<uint64_t>(r.w) << 32) | r.z;
     return Uniform2{u53_to_unit(a), u53_to_unit(b)};
