@@ -254,20 +254,21 @@ def reference_runner(config: str, R, cores: int, budget_s: float):
         f"{probe} walkers/obs via the reference's simulate_to_exit"
 
 
-def cpu_reference_sample(config: str, ctx, per_eval: float, budget_s: float = 6.0):
-    """cpu_baseline: 1 warm-up + median of 3 bounded runs
-    (benchmark.cpp:39-52 methodology) on all host cores."""
+def cpu_reference_sample(config: str, ctx, per_eval: float, budget_s: float = 4.0):
+    """cpu_baseline: 1 warm-up + median of 5 bounded runs
+    (benchmark.cpp:39-52 methodology; median of >= 5) on all
+    host cores."""
     from oracle.oracle import Reference
     R = Reference()
     cores = os.cpu_count() or 1
     steps, run, sample = reference_runner(config, R, cores, budget_s)
     run()
     times = []
-    for _ in range(3):
+    for _ in range(5):
         t0 = time.perf_counter()
         run()
         times.append(time.perf_counter() - t0)
-    return steps / statistics.median(times), cores, sample + ", median of 3 after 1 warm-up"
+    return steps / statistics.median(times), cores, sample + ", median of 5 after 1 warm-up"
 
 
 # ---------------------------------------------------------------------------
