@@ -31,12 +31,12 @@ template <int K, class T, int P, int MINB>
 __global__ void __launch_bounds__(kBlock, MINB) ad_particles_disk(const AdLaunch L, const double* coef) {
     // this sample's coefficient block -> shared memory (compute type)
     __shared__ __align__(16) T staged[DiskShape<K>::n_coef];
-    const int sample = blockIdx.z;
+    const int sample = L.obs_major ? blockIdx.y : blockIdx.z;
     const double* src = coef + static_cast<int64_t>(sample) * DiskShape<K>::n_coef;
     for (int i = threadIdx.x; i < DiskShape<K>::n_coef; i += kBlock) staged[i] = T(src[i]);
     __syncthreads();
     const SmemCoef<T> C{static_cast<uint32_t>(__cvta_generic_to_shared(staged))};
-    const int obs = blockIdx.y;
+    const int obs = __ldg(L.obs_order + (L.obs_major ? blockIdx.z : blockIdx.y));
     const int64_t span = L.p_end - L.p_begin;
     const int64_t base = static_cast<int64_t>(blockIdx.x) * kBlock * P + threadIdx.x;
     if (base >= span) return;
@@ -142,9 +142,14 @@ template <int K, class T, int P, int MINB>
 cudaError_t launch_k(const AdLaunch& L, const double* coef, cudaStream_t s) {
     const int64_t span = L.p_end - L.p_begin;
     const int64_t per_block = static_cast<int64_t>(kBlock) * P;
-    const dim3 grid(static_cast<unsigned>((span + per_block - 1) / per_block), static_cast<unsigned>(L.n_obs),
-                    static_cast<unsigned>(L.n_samples));
-    ad_particles_disk<K, T, P, MINB><<<grid, kBlock, 0, s>>>(L, coef);
+    const int64_t nb = (span + per_block - 1) / per_block;
+    AdLaunch LB = L;
+    LB.obs_major = batched_obs_major(L, nb);
+    const dim3 grid = LB.obs_major ? dim3(static_cast<unsigned>(nb), static_cast<unsigned>(L.n_samples),
+                                          static_cast<unsigned>(L.n_obs))
+                                   : dim3(static_cast<unsigned>(nb), static_cast<unsigned>(L.n_obs),
+                                          static_cast<unsigned>(L.n_samples));
+    ad_particles_disk<K, T, P, MINB><<<grid, kBlock, 0, s>>>(LB, coef);
     return cudaGetLastError();
 }
 

@@ -21,11 +21,13 @@ constexpr size_t kSmemLimit = 64 * 1024;   // tables up to here: 256-thread bloc
 constexpr size_t kSmemMax = 220 * 1024;    // larger tables: one 512-thread block per SM
 constexpr size_t kSmemHard = 227 * 1024;
 
-template <class T, bool SMEM, int kBlock>
+template <class T, bool SMEM, int kBlock, bool OM>
 __global__ void __launch_bounds__(kBlock, 512 / kBlock) ad_particles(const AdLaunch L) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int obs = blockIdx.y;
-    const int sample = blockIdx.z;
+    // OM: grid (particle blocks, samples, observations longest first);
+    // otherwise (particle blocks, observations, samples)
+    const int obs = OM ? __ldg(L.obs_order + blockIdx.z) : static_cast<int>(blockIdx.y);
+    const int sample = OM ? blockIdx.y : blockIdx.z;
     const LatticeImg& lat = L.vel.lat;
     const bool is_const = L.vel.is_constant;
     const double* gblock = lat.coef + static_cast<int64_t>(sample) * lat.sample_stride;
@@ -52,19 +54,28 @@ __global__ void __launch_bounds__(kBlock, 512 / kBlock) ad_particles(const AdLau
     });
 }
 
-template <class T, bool SMEM, int BS>
-void go(const AdLaunch& L, int64_t span, size_t smem, cudaStream_t s) {
-    const dim3 grid(static_cast<unsigned>((span + BS - 1) / BS), static_cast<unsigned>(L.n_obs),
-                    static_cast<unsigned>(L.n_samples));
+template <class T, bool SMEM, int BS, bool OM>
+void go_om(const AdLaunch& L, int64_t nb, size_t smem, cudaStream_t s) {
+    const dim3 grid = OM ? dim3(static_cast<unsigned>(nb), static_cast<unsigned>(L.n_samples),
+                                static_cast<unsigned>(L.n_obs))
+                         : dim3(static_cast<unsigned>(nb), static_cast<unsigned>(L.n_obs),
+                                static_cast<unsigned>(L.n_samples));
     if constexpr (SMEM) {
         static bool configured = false;
         if (!configured) {
-            cudaFuncSetAttribute(ad_particles<T, true, BS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaFuncSetAttribute(ad_particles<T, true, BS, OM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(kSmemHard));
             configured = true;
         }
     }
-    ad_particles<T, SMEM, BS><<<grid, BS, smem, s>>>(L);
+    ad_particles<T, SMEM, BS, OM><<<grid, BS, smem, s>>>(L);
+}
+
+template <class T, bool SMEM, int BS>
+void go(const AdLaunch& L, int64_t span, size_t smem, cudaStream_t s) {
+    const int64_t nb = (span + BS - 1) / BS;
+    if (batched_obs_major(L, nb)) go_om<T, SMEM, BS, true>(L, nb, smem, s);
+    else go_om<T, SMEM, BS, false>(L, nb, smem, s);
 }
 
 template <class T>
@@ -79,6 +90,30 @@ cudaError_t launch(const AdLaunch& L, cudaStream_t s) {
 }
 
 }  // namespace
+
+// Batched launches: observation-major with the longest observations first
+// (their blocks start in the first wave, the short ones fill the tail) when
+// the grid is a few waves; sample-major otherwise, so consecutive blocks
+// share a sample's coefficient block in L2.  SMC_BATCH_ORDER=obs|sample
+// forces one.
+int batched_obs_major(const AdLaunch& L, int64_t blocks_per_obs) {
+    const char* e = std::getenv("SMC_BATCH_ORDER");
+    if (e && e[0] == 'o') return 1;
+    if (e && e[0] == 's') return 0;
+    if (L.n_samples <= 1) return 0;
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    // pCN-sized launches (100 chains x 9 obs x 2 blocks = 1 800 blocks):
+    // 103 vs 117 us (K=2) and 266 vs 322 us (K=8) per chain step; C4 (147 456
+    // blocks) keeps the sample-major order
+    const int64_t blocks = blocks_per_obs * L.n_obs * static_cast<int64_t>(L.n_samples);
+    return blocks <= 32LL * sms ? 1 : 0;
+}
 
 cudaError_t launch_ad_particles(const AdLaunch& L, cudaStream_t s) { return launch<double>(L, s); }
 cudaError_t launch_ad_particles_fp32(const AdLaunch& L, cudaStream_t s) { return launch<float>(L, s); }

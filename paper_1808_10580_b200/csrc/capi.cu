@@ -120,6 +120,14 @@ AdPrepared prepare_ad(smc_ctx* ctx, const smc_ad_problem& p, const std::vector<c
         out.steps_per_particle_sum += obs.back().n_steps;
     }
     const size_t obs_off = im.add_vec(obs);
+    // batched launches schedule the longest observations first (grid z), so
+    // the short ones fill the tail instead of a long one trailing alone
+    std::vector<int32_t> order(obs.size());
+    for (size_t j = 0; j < order.size(); ++j) order[j] = static_cast<int32_t>(j);
+    if (std::getenv("SMC_NO_LPT") == nullptr)
+        std::stable_sort(order.begin(), order.end(),
+                         [&](int32_t a, int32_t b) { return obs[a].n_steps > obs[b].n_steps; });
+    const size_t order_off = im.add_vec(order);
     const ScalarRef th = add_scalar(im, p.initial_condition);
     const VelRef vr = add_velocity(im, structure, fills);
     // Dense fields with K <= kDiskMaxK take the compile-time disk kernel.
@@ -146,6 +154,7 @@ AdPrepared prepare_ad(smc_ctx* ctx, const smc_ad_problem& p, const std::vector<c
     L.vel = patch(vr, base);
     L.theta0 = patch(th, base);
     L.obs = reinterpret_cast<const AdObsImg*>(base + obs_off);
+    L.obs_order = reinterpret_cast<const int32_t*>(base + order_off);
     L.n_obs = static_cast<int32_t>(obs_count);
     L.obs_slot0 = static_cast<uint32_t>(obs_begin);
     L.n_particles = p.n_particles;

@@ -33,10 +33,15 @@ struct AdLaunch {
     double sigma;              // sqrt(2 kappa)
     double* values;            // [n_samples][n_obs][p_end - p_begin]
     const double* host_disk;   // host copy of the single-sample disk coefficient block (or null)
+    const int32_t* obs_order;  // [n_obs] observations by decreasing step count
+    int32_t obs_major;         // batched grid order: 1 = (blocks, samples, obs longest first), 0 = (blocks, obs, samples)
+    int32_t pad_;
     RoundKeys rk;              // Philox round keys of `seed` (filled by the launcher that uses them)
 };
 
 cudaError_t launch_ad_particles(const AdLaunch& L, cudaStream_t s);
+// Batched grid order (AdLaunch::obs_major) for a launch of this shape.
+int batched_obs_major(const AdLaunch& L, int64_t blocks_per_obs);
 cudaError_t launch_ad_particles_fp32(const AdLaunch& L, cudaStream_t s);
 cudaError_t launch_ad_particles_strict(const AdLaunch& L, cudaStream_t s);
 
