@@ -49,6 +49,38 @@ __global__ void __launch_bounds__(kBlock, MINB) ad_particles_disk(const AdLaunch
                          });
 }
 
+// Observation-major batched launches with >= 64 particles per observation
+// (pCN: 100 chains x 160 particles): the threads of one observation run over
+// the flattened (sample, particle) range, so every block is full (160
+// particles per sample filled one 4-warp and one 1-warp block before) and
+// stages the <= 3 consecutive sample blocks its threads touch.  Warps stay
+// within one sample when the particle count is a multiple of 32.
+template <int K, class T, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) ad_particles_disk_flat(const AdLaunch L, const double* coef) {
+    constexpr int NC = DiskShape<K>::n_coef;
+    constexpr int kMaxSamples = 3;
+    __shared__ __align__(16) T staged[kMaxSamples * NC];
+    const int64_t span = L.p_end - L.p_begin;
+    const int64_t total = span * L.n_samples;
+    const int64_t flat0 = static_cast<int64_t>(blockIdx.x) * kBlock;
+    const int s0 = static_cast<int>(flat0 / span);
+    const int64_t last = (flat0 + kBlock < total ? flat0 + kBlock : total) - 1;
+    const int ns = static_cast<int>(last / span) - s0 + 1;
+    const double* src = coef + static_cast<int64_t>(s0) * NC;  // sample blocks are contiguous
+    for (int i = threadIdx.x; i < ns * NC; i += kBlock) staged[i] = T(src[i]);
+    __syncthreads();
+    const int64_t flat = flat0 + threadIdx.x;
+    if (flat >= total) return;
+    const int sample = static_cast<int>(flat / span);
+    int64_t local[1] = {flat - static_cast<int64_t>(sample) * span};
+    const int obs = __ldg(L.obs_order + blockIdx.y);
+    const SmemCoef<T> C{static_cast<uint32_t>(__cvta_generic_to_shared(staged + (sample - s0) * NC))};
+    ad_particles_p<T, 1>(L, obs, sample, local, span,
+                         [&](const T (&x1)[1], const T (&x2)[1], T (&v1)[1], T (&v2)[1], int) {
+                             velocity_disk<K, T, 1>(C, x1, x2, v1, v2);
+                         });
+}
+
 // Single-sample launches take the coefficient block as a KERNEL PARAMETER
 // (constant bank 0, per launch, so concurrent contexts cannot race): the
 // DFMAs then read their coefficient through uniform registers (LDCU), which
@@ -145,6 +177,14 @@ cudaError_t launch_k(const AdLaunch& L, const double* coef, cudaStream_t s) {
     const int64_t nb = (span + per_block - 1) / per_block;
     AdLaunch LB = L;
     LB.obs_major = batched_obs_major(L, nb);
+    if constexpr (P == 1) {
+        if (LB.obs_major && span >= 64 && std::getenv("SMC_NO_FLAT") == nullptr) {
+            const int64_t total = span * L.n_samples;
+            const dim3 fgrid(static_cast<unsigned>((total + kBlock - 1) / kBlock), static_cast<unsigned>(L.n_obs), 1);
+            ad_particles_disk_flat<K, T, MINB><<<fgrid, kBlock, 0, s>>>(LB, coef);
+            return cudaGetLastError();
+        }
+    }
     const dim3 grid = LB.obs_major ? dim3(static_cast<unsigned>(nb), static_cast<unsigned>(L.n_samples),
                                           static_cast<unsigned>(L.n_obs))
                                    : dim3(static_cast<unsigned>(nb), static_cast<unsigned>(L.n_obs),
