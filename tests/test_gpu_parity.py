@@ -321,6 +321,22 @@ def test_fp32_param_path_matches_shared_memory_path(ctx, golden, monkeypatch):
         assert np.array_equal(x, y), float(np.max(np.abs(x - y)))
 
 
+@pytest.mark.parametrize("K", [1, 5, 12])
+def test_fp32_param_path_matches_batched_path(ctx, K):
+    """The packed FP32 kernel-parameter form (FFMA2) against the batched
+    shared-memory kernel on the same single sample, across the disk sizes:
+    identical estimates."""
+    prior = S.PriorSpec(K, 1.0, 2.5)
+    u = np.random.default_rng(100 + K).normal(size=prior.dimension()) * 0.4
+    base = specs.c4_base(n_particles=1000, precision=S.Precision.fp32)
+    batched = S.observe_ad_batched(base, prior, u[None, :], 77, ctx=ctx)
+    spec = specs.c4_base(n_particles=1000, precision=S.Precision.fp32)
+    spec.velocity = S.VelocityField.fourier(S.velocity_from_coefficients(prior, u))
+    single = S.observe_ad(spec, 77, ctx=ctx)
+    for j, e in enumerate(single):
+        assert batched[0, j]["mean"] == e.mean and batched[0, j]["std_error"] == e.std_error, j
+
+
 # ---------------------------------------------------------------- BVP ------
 def test_bvp_box_matches_reference(ctx, golden):
     g = golden["bvp_box"]
