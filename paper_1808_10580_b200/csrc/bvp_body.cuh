@@ -65,6 +65,20 @@ struct Forcing {
             phi[i] = SMC_SCALAR_EXP(neg_a * (d1 * d1 + d2 * d2));
         }
     }
+    // FP32 variant (3-SE gate): the bump sum in float with the SFU exponential
+    __device__ __forceinline__ float operator()(const ScalarImg& f, float x1, float x2) const {
+        if constexpr (NB == 0) {
+            return float(scalar_eval(f, double(x1), double(x2)));
+        } else {
+            float s = 0.0f;
+#pragma unroll
+            for (int i = 0; i < NB; ++i) {
+                const float d1 = x1 - float(c1[i]), d2 = x2 - float(c2[i]);
+                s = fmaf(float(amp[i]), __expf(float(neg_a) * fmaf(d1, d1, d2 * d2)), s);
+            }
+            return s;
+        }
+    }
     __device__ __forceinline__ double operator()(const ScalarImg& f, double x1, double x2) const {
         if constexpr (NB == 0) {
             return scalar_eval(f, x1, x2);
@@ -181,7 +195,7 @@ __global__ void __launch_bounds__(kBvpBlock) bvp_walkers(const BvpLaunch L) {
             T f = T(0);
             double phi[NB > 0 ? NB : 1];
             if constexpr (BASIS) forcing.basis(double(x1), double(x2), phi);
-            else f = T(forcing(L.forcing, double(x1), double(x2)));
+            else f = forcing(L.forcing, x1, x2);  // FP64, or the float variant for T = float
             ++my_steps;
             if (!domain_contains<T>(L.domain, n1, n2)) {
                 T h1, h2;
