@@ -22,7 +22,13 @@ namespace smc {
 constexpr int kLatticeTile = 8;
 
 __device__ __forceinline__ void sincospi_t(double a, double* s, double* c) { fm::sincospi(a, s, c); }
-__device__ __forceinline__ void sincospi_t(float a, float* s, float* c) { sincospif(a, s, c); }
+// FP32 variant (3-SE gate): reduce to [-1, 1] and use the SFU sine/cosine
+// (absolute error ~2^-21 on [-pi, pi]), which moves the work off the FMA pipe
+// the FP32 kernels are bound by.
+__device__ __forceinline__ void sincospi_t(float a, float* s, float* c) {
+    const float r = fmaf(-2.0f, rintf(0.5f * a), a);  // a - 2 round(a / 2), exact
+    __sincosf(3.14159265f * r, s, c);
+}
 
 // Four coefficients (alpha_re, alpha_im, beta_re, beta_im) of one pair.
 template <class T>
