@@ -61,12 +61,13 @@ void go_om(const AdLaunch& L, int64_t nb, size_t smem, cudaStream_t s) {
                          : dim3(static_cast<unsigned>(nb), static_cast<unsigned>(L.n_obs),
                                 static_cast<unsigned>(L.n_samples));
     if constexpr (SMEM) {
-        static bool configured = false;
-        if (!configured) {
+        // once per instantiation (thread-safe static initialisation)
+        static const bool configured = [] {
             cudaFuncSetAttribute(ad_particles<T, true, BS, OM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(kSmemHard));
-            configured = true;
-        }
+            return true;
+        }();
+        (void)configured;
     }
     ad_particles<T, SMEM, BS, OM><<<grid, BS, smem, s>>>(L);
 }
@@ -101,13 +102,12 @@ int batched_obs_major(const AdLaunch& L, int64_t blocks_per_obs) {
     if (e && e[0] == 'o') return 1;
     if (e && e[0] == 's') return 0;
     if (L.n_samples <= 1) return 0;
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
+    static const int sms = [] {
+        int dev = 0, n = 0;
         cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        return n > 0 ? n : 148;
+    }();
     // pCN-sized launches (100 chains x 9 obs x 2 blocks = 1 800 blocks):
     // 103 vs 117 us (K=2) and 266 vs 322 us (K=8) per chain step; C4 (147 456
     // blocks) keeps the sample-major order
