@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <mutex>
 
 #include "ad_body.cuh"
 
@@ -20,6 +21,7 @@ namespace {
 constexpr size_t kSmemLimit = 64 * 1024;   // tables up to here: 256-thread blocks, 2 per SM
 constexpr size_t kSmemMax = 220 * 1024;    // larger tables: one 512-thread block per SM
 constexpr size_t kSmemHard = 227 * 1024;
+constexpr int kMaxDevices = 64;
 
 template <class T, bool SMEM, int kBlock, bool OM>
 __global__ void __launch_bounds__(kBlock, 512 / kBlock) ad_particles(const AdLaunch L) {
@@ -61,13 +63,16 @@ void go_om(const AdLaunch& L, int64_t nb, size_t smem, cudaStream_t s) {
                          : dim3(static_cast<unsigned>(nb), static_cast<unsigned>(L.n_obs),
                                 static_cast<unsigned>(L.n_samples));
     if constexpr (SMEM) {
-        // once per instantiation (thread-safe static initialisation)
-        static const bool configured = [] {
+        // once per instantiation and device (the attribute is per device)
+        static std::once_flag flags[kMaxDevices];
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const auto configure = [] {
             cudaFuncSetAttribute(ad_particles<T, true, BS, OM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(kSmemHard));
-            return true;
-        }();
-        (void)configured;
+        };
+        if (dev >= 0 && dev < kMaxDevices) std::call_once(flags[dev], configure);
+        else configure();
     }
     ad_particles<T, SMEM, BS, OM><<<grid, BS, smem, s>>>(L);
 }
