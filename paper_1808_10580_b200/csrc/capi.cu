@@ -238,17 +238,29 @@ void ad_observe_range(smc_ctx* ctx, const smc_ad_problem& p, uint64_t seed, int6
     check_scalar(p.initial_condition);
     ad_validate(p);
     check_particle_range(p.n_particles);
-    ctx->stats = smc_stats{};
-    AdPrepared P = prepare_ad(ctx, p, {&v}, v, obs_begin, obs_count);
-    P.L.seed = seed;
-    const int64_t n = p.n_particles;
-    P.L.values = ctx->values.get<double>(static_cast<size_t>(obs_count * n));
-    CK(cudaEventRecord(ctx->ev[0], ctx->stream));
-    run_particles(ctx, P.L, &P);
-    CK(cudaEventRecord(ctx->ev[1], ctx->stream));
-    reduce_ad(ctx, P.L.values, n, obs_count, out);
-    finish_stats(ctx);
-    ctx->stats.particle_steps = P.steps_per_particle_sum * n;
+    smc_stats total{};
+    // observations index a grid dimension (<= 65535 per launch); larger sets
+    // run in chunks — each observation's estimate depends only on its own
+    // slot, so chunking does not change results
+    constexpr int64_t kMaxObsPerLaunch = 65535;
+    for (int64_t b = obs_begin; b < obs_begin + obs_count; b += kMaxObsPerLaunch) {
+        const int64_t cnt = std::min(kMaxObsPerLaunch, obs_begin + obs_count - b);
+        ctx->stats = smc_stats{};
+        AdPrepared P = prepare_ad(ctx, p, {&v}, v, b, cnt);
+        P.L.seed = seed;
+        const int64_t n = p.n_particles;
+        P.L.values = ctx->values.get<double>(static_cast<size_t>(cnt * n));
+        CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+        run_particles(ctx, P.L, &P);
+        CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+        reduce_ad(ctx, P.L.values, n, cnt, out + (b - obs_begin));
+        finish_stats(ctx);
+        total.particle_kernel_ms += ctx->stats.particle_kernel_ms;
+        total.reduce_ms += ctx->stats.reduce_ms;
+        total.kernel_launches += ctx->stats.kernel_launches;
+        total.particle_steps += P.steps_per_particle_sum * n;
+    }
+    ctx->stats = total;
 }
 
 BvpLaunch prepare_bvp(smc_ctx* ctx, const smc_bvp_problem& p, int64_t obs_begin, int64_t obs_count) {

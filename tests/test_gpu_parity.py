@@ -293,6 +293,22 @@ def test_sharded_partials_are_bit_identical(ctx, world):
         assert a.mean == b.mean and a.std_error == b.std_error
 
 
+def test_more_observations_than_one_grid_dimension(ctx):
+    """70 000 observations (> 65 535, one grid dimension) run in chunks; each
+    estimate depends only on its own observation slot, so it equals the
+    single-observation call for that slot in either chunk."""
+    rng = np.random.default_rng(5)
+    xs = rng.random((70000, 2))
+    spec = S.AdProblemSpec(diffusion=S.DiffusionModel.isotropic(0.02),
+                           initial_condition=S.ScalarField.cosine_mode(1, 1, 1.0),
+                           observations=[S.AdObservation(0.01, S.Vec2(*x)) for x in xs], n_particles=4, dt=0.005)
+    est = S.observe_ad(spec, 9, ctx=ctx)
+    assert len(est) == 70000
+    for j in (0, 65534, 65535, 69999):
+        one = S.observe_ad_single(spec, j, 9, ctx=ctx)
+        assert one.mean == est[j].mean and one.std_error == est[j].std_error, j
+
+
 # ---------------------------------------------------------------- FP32 -----
 def test_fp32_within_three_standard_errors(ctx, golden):
     spec = specs.c1_two_mode(n_particles=10000, precision=S.Precision.fp32)
