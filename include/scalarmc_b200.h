@@ -178,7 +178,8 @@ smc_status smc_ad_observe_single(smc_ctx* ctx, const smc_ad_problem* prob, uint6
  * (inference.cpp:63-73) turns into a field, so row b reproduces
  * LikelihoodSpec::misfit's observe_ad call (inference.cpp:93-104) for u_b.
  * seeds: [B], or NULL for common random numbers (every sample uses `seed`).
- * The velocity slot of `base` is ignored. out: [B][n_obs]. */
+ * The velocity slot of `base` is ignored. out: [B][n_obs].  At most 65535
+ * observations per call (one grid dimension; smc_ad_observe has no limit). */
 smc_status smc_ad_observe_batched(smc_ctx* ctx, const smc_ad_problem* base, const smc_prior* prior,
                                   int64_t n_samples, const double* u, const uint64_t* seeds,
                                   uint64_t seed, smc_estimate* out);

@@ -490,6 +490,7 @@ smc_status smc_ad_shard_partials(smc_ctx* ctx, const smc_ad_problem* p, uint64_t
         const int64_t n_chunks = smc_num_chunks(p->n_particles);
         if (chunk_begin < 0 || chunk_end > n_chunks || chunk_begin > chunk_end)
             raise(SMC_ERANGE, "smc_ad_shard_partials: chunk range out of bounds");
+        if (p->n_obs > 65535) raise(SMC_ERUNTIME, "smc_ad_shard_partials: at most 65535 observations per shard launch");
         ctx->stats = smc_stats{};
         AdPrepared P = prepare_ad(ctx, *p, {&v}, v, 0, p->n_obs);
         P.L.seed = seed;

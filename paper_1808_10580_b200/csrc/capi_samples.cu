@@ -24,6 +24,8 @@ smc_status smc_ad_observe_batched(smc_ctx* ctx, const smc_ad_problem* base, cons
         ad_validate(p);
         check_particle_range(p.n_particles);
         if (p.precision == SMC_FP64_STRICT) raise(SMC_EINVAL, "strict precision is single-sample only");
+        if (p.n_obs > 65535)
+            raise(SMC_ERUNTIME, "observe_ad_batched: at most 65535 observations per batched launch");
         ctx->stats = smc_stats{};
         const int64_t n = p.n_particles, n_obs = p.n_obs;
         // One FourierVelocityField per sample from u in prior order
@@ -136,6 +138,8 @@ smc_status smc_pcn_chains(smc_ctx* ctx, const smc_ad_problem* forward, const smc
         const PackMap pmap = pack_map(prior->cutoff, use_disk, &Lh);
         const int64_t stride = pmap.stride;
         if (!prior_only && static_cast<int64_t>(p.n_obs) <= 0) raise(SMC_EINVAL, "AdProblemSpec: no observations");
+        if (!prior_only && p.n_obs > 65535)
+            raise(SMC_ERUNTIME, "smc_pcn_chains: at most 65535 observations in the likelihood's forward map");
 
         // device buffers (freed at the end of the call)
         std::vector<void*> owned;
