@@ -459,9 +459,9 @@ def run_ours(args):
                          "flops_per_unit": F, "unit_of_work": "particle-step",
                          "flops_note": "algorithmic flops = SURVEY.md 8(d) F_AD (the reference's 14 flops per "
                                        "mode); the kernels execute fewer (4 FMA per mode, Chebyshev "
-                                       "harmonics), so frac can exceed 1 — the pipe utilisation is ncu's "
-                                       + ("fma_pipe_pct_active in profiles/r01_k1_<config>_fp32.md" if fp32 else
-                                          "fp64_pipe_pct_active in profiles/r01_k1_<config>.md"),
+                                       "harmonics), so frac can exceed 1 — the hardware figure is "
+                                       "traffic.pipe_active_frac, ncu's active fraction of the dominant pipe "
+                                       "for this kernel",
                          "traffic": _ncu_traffic(args.config + ("_fp32" if fp32 else ""))},
             "gpu_launches": launches,
             "clocks": clocks,
@@ -492,13 +492,19 @@ def _image_bytes(spec) -> int:
 
 
 def _ncu_traffic(config: str = "c2"):
-    """DRAM bytes per particle-kernel launch from the committed ncu --set full
-    capture of this config (profiles/rNN_k*_<config>.json), if any."""
-    caps = sorted(PROFILES.glob(f"r*_k*_{config}.json"))
+    """DRAM bytes per particle-kernel launch and the dominant pipe's active
+    fraction from the committed ncu --set full capture of this config
+    (profiles/rNN_k*_<config>[_reduced].json), if any."""
+    caps = sorted(PROFILES.glob(f"r*_k*_{config}.json")) or sorted(PROFILES.glob(f"r*_k*_{config}_reduced.json"))
     if caps:
         try:
             d = json.loads(caps[-1].read_text())
-            return {"dram_bytes_per_launch": d.get("dram_bytes_per_launch"), "source": f"profiles/{caps[-1].name}"}
+            fp32 = config.endswith("_fp32")
+            pipe = d.get("fma_pipe_pct_active" if fp32 else "fp64_pipe_pct_active")
+            return {"dram_bytes_per_launch": d.get("dram_bytes_per_launch"), "source": f"profiles/{caps[-1].name}",
+                    "pipe": "fma (FP32)" if fp32 else "fp64",
+                    "pipe_active_frac": None if pipe is None else round(pipe / 100.0, 4),
+                    "reduced_launch": caps[-1].name.endswith("_reduced.json")}
         except Exception:  # noqa: BLE001
             return None
     return None
