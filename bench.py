@@ -354,21 +354,40 @@ def run_ours(args):
     elif kind == "bvp":
         spec = payload
         n_obs = len(spec.observations)
-        ob, oe = (n_obs * rank) // world, (n_obs * (rank + 1)) // world
+        if world == 1:
+            def device_step():
+                def run():
+                    S.observe_bvp(spec, 606, ctx=ctx)
+                    st = ctx.stats()
+                    return st.particle_kernel_ms, st.particle_steps
+                return timed(run)
 
-        def device_step():
-            def run():
-                S.observe_bvp_range(spec, 606, ob, oe - ob, ctx=ctx)
-                st = ctx.stats()
-                return st.particle_kernel_ms, st.particle_steps
-            return timed(run)
+            def e2e_step():
+                return S.observe_bvp(spec, 606, ctx=ctx)
+            api = "paper_1808_10580_b200.observe_bvp -> smc_bvp_observe (C ABI)"
+        else:  # walker sharding: every rank runs its walker range of all observations
+            bops = D.BvpDeviceOps(spec, 606, ctx)
+            wb, we = D.walker_range(spec.n_particles, rank, world)
+            wcounts = [D.walker_range(spec.n_particles, r, world)[1] - D.walker_range(spec.n_particles, r, world)[0]
+                       for r in range(world)]
 
-        def e2e_step():
-            return S.observe_bvp_range(spec, 606, ob, oe - ob, ctx=ctx)
-        api = "paper_1808_10580_b200.observe_bvp_range -> smc_bvp_observe_range (C ABI)"
-        parallel = f"observation-shard x{world}" if world > 1 else "single GPU"
+            def device_step():
+                def run():
+                    vals, aux, failed = bops.shard(wb, we)
+                    st = ctx.stats()
+                    k, steps = st.particle_kernel_ms, st.particle_steps
+                    bops.reduce(bops.all_gather(vals, wcounts), bops.all_gather(aux, wcounts),
+                                bops.all_gather(failed, wcounts))
+                    return k, steps
+                return timed(run)
+
+            def e2e_step():
+                return D.observe_bvp_sharded(spec, 606, rank, world, ctx)
+            api = ("paper_1808_10580_b200.distributed.observe_bvp_sharded (C ABI smc_bvp_shard_values + "
+                   "all-gather of walker results + smc_bvp_reduce_values)")
+        parallel = f"walker-shard x{world}" if world > 1 else "single GPU"
         scaling = "strong"
-        h2d, d2h = 16 * n_obs + 512, 40 * (oe - ob)
+        h2d, d2h = 16 * n_obs + 512, 40 * n_obs
         kernel_name = "bvp_walkers (K2)"
     else:  # batched
         base, prior, U = payload

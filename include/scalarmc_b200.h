@@ -196,6 +196,23 @@ smc_status smc_bvp_observe(smc_ctx* ctx, const smc_bvp_problem* prob, uint64_t s
 smc_status smc_bvp_observe_range(smc_ctx* ctx, const smc_bvp_problem* prob, uint64_t seed, int64_t obs_begin,
                                  int64_t obs_count, smc_estimate* out);
 
+/* Walker sharding of one Dirichlet evaluation: run walkers
+ * [walker_begin, walker_end) of every observation (their own stream keys, so
+ * the results do not depend on the split) and write the per-walker results
+ * to caller-owned DEVICE arrays [n_obs][walker_end - walker_begin]: value
+ * (theta_bc(X_tau) - int f), exit time, failed flag.  The ranks then
+ * all-gather the arrays (rank order = walker order) and reduce the whole
+ * [n_obs][n_particles] set with smc_bvp_reduce_values, which reproduces
+ * observe_bvp bit for bit for any split: the reference's compaction of valid
+ * walkers depends on failures anywhere before a walker, so the exchange
+ * carries walker results rather than partial sums. */
+smc_status smc_bvp_shard_values(smc_ctx* ctx, const smc_bvp_problem* prob, uint64_t seed, int64_t walker_begin,
+                                int64_t walker_end, double* values_dev, double* aux_dev, uint8_t* failed_dev);
+/* reduce_observation (executor.cpp:87-117) of device arrays
+ * [n_obs][n_walkers]; out: [n_obs] on the host. */
+smc_status smc_bvp_reduce_values(smc_ctx* ctx, const double* values_dev, const double* aux_dev,
+                                 const uint8_t* failed_dev, int64_t n_walkers, int64_t n_obs, smc_estimate* out);
+
 /* Forcing basis of the Dirichlet map.  With common
  * random numbers the walker paths do not depend on the forcing amplitudes F,
  * so for a Gaussian-bump forcing (1..4 bumps; the amplitudes in `prob` are

@@ -123,6 +123,10 @@ _PROTOS = {
                                   C.POINTER(smc_estimate)]),
     "smc_bvp_observe_range": (C.c_int, [C.c_void_p, C.POINTER(smc_bvp_problem), C.c_uint64, C.c_int64,
                                         C.c_int64, C.POINTER(smc_estimate)]),
+    "smc_bvp_shard_values": (C.c_int, [C.c_void_p, C.POINTER(smc_bvp_problem), C.c_uint64, C.c_int64, C.c_int64,
+                                       C.c_void_p, C.c_void_p, C.c_void_p]),
+    "smc_bvp_reduce_values": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+                                        C.POINTER(smc_estimate)]),
     "smc_bvp_forcing_basis": (C.c_int, [C.c_void_p, C.POINTER(smc_bvp_problem), C.c_uint64, _dp, _dp, _dp,
                                         C.POINTER(C.c_int64)]),
     "smc_pcn_num_samples": (C.c_int64, [C.POINTER(smc_chain_config)]),

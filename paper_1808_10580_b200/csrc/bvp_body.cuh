@@ -141,7 +141,8 @@ __global__ void __launch_bounds__(kBvpBlock) bvp_walkers(const BvpLaunch L) {
                     if (idx < total) {
                         w = idx;
                         obs = static_cast<uint32_t>(idx / static_cast<unsigned long long>(L.n_particles));
-                        particle = static_cast<uint32_t>(idx - static_cast<unsigned long long>(obs) * L.n_particles);
+                        particle = static_cast<uint32_t>(L.p_begin + static_cast<int64_t>(
+                                       idx - static_cast<unsigned long long>(obs) * L.n_particles));
                         x1 = T(__ldg(L.obs_x + 2 * obs));
                         x2 = T(__ldg(L.obs_x + 2 * obs + 1));
                         f_int = T(0);

@@ -635,6 +635,47 @@ smc_status smc_bvp_observe(smc_ctx* ctx, const smc_bvp_problem* p, uint64_t seed
     return smc_bvp_observe_range(ctx, p, seed, 0, p->n_obs, out);
 }
 
+// reduce_observation for every observation of [n_obs][n] walker results on
+// the device (executor.cpp:87-117): stable compaction of the valid walkers,
+// then the same trees as AD; estimates to the host.  step_total (device,
+// optional): the walker-step counter to report in the stats.
+static void reduce_bvp(smc_ctx* ctx, const double* values, const double* aux, const uint8_t* failed, int64_t n,
+                       int64_t n_obs, const unsigned long long* step_total, smc_estimate* out) {
+    cudaStream_t s = ctx->stream;
+    const int64_t chunks = smc_num_chunks(n);
+    double* cvalues = ctx->tmp_a.get<double>(static_cast<size_t>(n_obs * n));
+    double* caux = ctx->tmp_b.get<double>(static_cast<size_t>(n_obs * n));
+    int64_t* chunk_tmp = ctx->tmp_c.get<int64_t>(static_cast<size_t>(2 * n_obs * chunks));
+    int64_t* counts = ctx->counts.get<int64_t>(static_cast<size_t>(n_obs));
+    CK(compact_valid(values, aux, failed, n, n_obs, cvalues, caux, counts, chunk_tmp, s));
+    double* scratch = ctx->scratch.get<double>(static_cast<size_t>(2 * n_obs * std::max<int64_t>(chunks, 1)));
+    double* sums = ctx->sums.get<double>(static_cast<size_t>(n_obs));
+    double* means = ctx->means.get<double>(static_cast<size_t>(n_obs));
+    double* sumsq = ctx->sumsq.get<double>(static_cast<size_t>(n_obs));
+    double* sumaux = ctx->sumaux.get<double>(static_cast<size_t>(n_obs));
+    smc_estimate* est = ctx->est.get<smc_estimate>(static_cast<size_t>(n_obs));
+    int launches = 3;
+    CK(tree_reduce(cvalues, n, counts, n, n_obs, sums, nullptr, 0, scratch, s, &launches));
+    CK(launch_divide(sums, counts, n, n_obs, means, s));
+    CK(tree_reduce(cvalues, n, counts, n, n_obs, sumsq, means, 1, scratch, s, &launches));
+    CK(tree_reduce(caux, n, counts, n, n_obs, sumaux, nullptr, 0, scratch, s, &launches));
+    CK(launch_estimates(means, sumsq, sumaux, counts, n, n, n_obs, est, s));
+    count_launches(ctx, launches + 2);
+    smc_estimate* h = ctx->est_host.get<smc_estimate>(static_cast<size_t>(n_obs));
+    CK(cudaMemcpyAsync(h, est, sizeof(smc_estimate) * n_obs, cudaMemcpyDeviceToHost, s));
+    unsigned long long* steps_h = ctx->staging.get<unsigned long long>(1);
+    *steps_h = 0;
+    if (step_total)
+        CK(cudaMemcpyAsync(steps_h, step_total, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(ctx->ev[2], s));
+    CK(cudaStreamSynchronize(s));
+    if (step_total) ctx->stats.particle_steps = static_cast<int64_t>(*steps_h);
+    finish_stats(ctx);
+    for (int64_t j = 0; j < n_obs; ++j)
+        if (h[j].n_failed == n) raise(SMC_ERUNTIME, "map_reduce: every particle of an observation failed");
+    std::memcpy(out, h, sizeof(smc_estimate) * n_obs);
+}
+
 smc_status smc_bvp_observe_range(smc_ctx* ctx, const smc_bvp_problem* p, uint64_t seed, int64_t obs_begin,
                                  int64_t obs_count, smc_estimate* out) {
     return guarded([&] {
@@ -646,38 +687,48 @@ smc_status smc_bvp_observe_range(smc_ctx* ctx, const smc_bvp_problem* p, uint64_
         L.seed = seed;
         const int64_t n = p->n_particles, n_obs = obs_count;
         run_bvp(ctx, L, n_obs, n);
-        // compaction of valid walkers, then the same tree as AD
+        reduce_bvp(ctx, L.values, L.aux, L.failed, n, n_obs, L.step_total, out);
+    });
+}
+
+smc_status smc_bvp_shard_values(smc_ctx* ctx, const smc_bvp_problem* p, uint64_t seed, int64_t walker_begin,
+                                int64_t walker_end, double* values_dev, double* aux_dev, uint8_t* failed_dev) {
+    return guarded([&] {
+        if (walker_begin < 0 || walker_end > p->n_particles || walker_begin > walker_end)
+            raise(SMC_ERANGE, "smc_bvp_shard_values: walker range out of bounds");
+        CK(cudaSetDevice(ctx->device));
+        ctx->stats = smc_stats{};
+        BvpLaunch L = prepare_bvp(ctx, *p, 0, p->n_obs);
+        L.seed = seed;
+        const int64_t span = walker_end - walker_begin;
+        if (span == 0) return;
+        L.n_particles = span;
+        L.p_begin = walker_begin;
+        run_bvp(ctx, L, p->n_obs, span);
         cudaStream_t s = ctx->stream;
-        const int64_t chunks = smc_num_chunks(n);
-        double* cvalues = ctx->tmp_a.get<double>(static_cast<size_t>(n_obs * n));
-        double* caux = ctx->tmp_b.get<double>(static_cast<size_t>(n_obs * n));
-        int64_t* chunk_tmp = ctx->tmp_c.get<int64_t>(static_cast<size_t>(2 * n_obs * chunks));
-        int64_t* counts = ctx->counts.get<int64_t>(static_cast<size_t>(n_obs));
-        CK(compact_valid(L.values, L.aux, L.failed, n, n_obs, cvalues, caux, counts, chunk_tmp, s));
-        double* scratch = ctx->scratch.get<double>(static_cast<size_t>(2 * n_obs * std::max<int64_t>(chunks, 1)));
-        double* sums = ctx->sums.get<double>(static_cast<size_t>(n_obs));
-        double* means = ctx->means.get<double>(static_cast<size_t>(n_obs));
-        double* sumsq = ctx->sumsq.get<double>(static_cast<size_t>(n_obs));
-        double* sumaux = ctx->sumaux.get<double>(static_cast<size_t>(n_obs));
-        smc_estimate* est = ctx->est.get<smc_estimate>(static_cast<size_t>(n_obs));
-        int launches = 3;
-        CK(tree_reduce(cvalues, n, counts, n, n_obs, sums, nullptr, 0, scratch, s, &launches));
-        CK(launch_divide(sums, counts, n, n_obs, means, s));
-        CK(tree_reduce(cvalues, n, counts, n, n_obs, sumsq, means, 1, scratch, s, &launches));
-        CK(tree_reduce(caux, n, counts, n, n_obs, sumaux, nullptr, 0, scratch, s, &launches));
-        CK(launch_estimates(means, sumsq, sumaux, counts, n, n, n_obs, est, s));
-        count_launches(ctx, launches + 2);
-        smc_estimate* h = ctx->est_host.get<smc_estimate>(static_cast<size_t>(n_obs));
-        CK(cudaMemcpyAsync(h, est, sizeof(smc_estimate) * n_obs, cudaMemcpyDeviceToHost, s));
+        const size_t total = static_cast<size_t>(p->n_obs * span);
+        CK(cudaMemcpyAsync(values_dev, L.values, total * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(aux_dev, L.aux, total * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(failed_dev, L.failed, total, cudaMemcpyDeviceToDevice, s));
         unsigned long long* steps_h = ctx->staging.get<unsigned long long>(1);
         CK(cudaMemcpyAsync(steps_h, L.step_total, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
         CK(cudaEventRecord(ctx->ev[2], s));
         CK(cudaStreamSynchronize(s));
         ctx->stats.particle_steps = static_cast<int64_t>(*steps_h);
         finish_stats(ctx);
-        for (int64_t j = 0; j < n_obs; ++j)
-            if (h[j].n_failed == n) raise(SMC_ERUNTIME, "map_reduce: every particle of an observation failed");
-        std::memcpy(out, h, sizeof(smc_estimate) * n_obs);
+    });
+}
+
+smc_status smc_bvp_reduce_values(smc_ctx* ctx, const double* values_dev, const double* aux_dev,
+                                 const uint8_t* failed_dev, int64_t n_walkers, int64_t n_obs, smc_estimate* out) {
+    return guarded([&] {
+        if (n_walkers < 2 || n_obs < 1)
+            raise(SMC_EINVAL, "smc_bvp_reduce_values: need >= 2 walkers and >= 1 observation");
+        CK(cudaSetDevice(ctx->device));
+        ctx->stats = smc_stats{};
+        CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+        CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+        reduce_bvp(ctx, values_dev, aux_dev, failed_dev, n_walkers, n_obs, nullptr, out);
     });
 }
 

@@ -62,7 +62,7 @@ struct BvpLaunch {
     int32_t n_obs;
     uint32_t obs_slot0;
     uint64_t seed;
-    int64_t n_particles;       // walkers per observation launched (particles [0, n))
+    int64_t n_particles;       // walkers per observation launched: particles [p_begin, p_begin + n)
     int64_t max_steps;
     double dt, root_dt, sigma, sr;  // sr = sigma * sqrt(dt)
     int32_t precision;
@@ -76,6 +76,7 @@ struct BvpLaunch {
     const double* disk_coef;   // disk_shape.h coefficient block when disk_K > 0
     int32_t disk_K;            // > 0: dense Fourier velocity on |k| <= disk_K (FP64 walkers use bvp_disk.cu)
     int32_t pad2_;
+    int64_t p_begin;           // first walker index of this launch (walker sharding; 0 otherwise)
     RoundKeys rk;              // Philox round keys of `seed` (with_round_keys, set by every K2 launcher)
 };
 

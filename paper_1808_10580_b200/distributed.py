@@ -13,6 +13,11 @@ bit-identical for any world size, including 1.
 Sample sharding for batched evaluation needs no collective: rank r evaluates
 its contiguous block of parameter samples.
 
+Walker sharding for a single Dirichlet evaluation (observe_bvp_sharded): rank
+r runs its walker range of every observation; the per-walker results are
+all-gathered in walker order and reduced once (the reference compacts valid
+walkers before its tree, so partial sums would not be split-invariant).
+
 The exchange logic is written against a small `ShardOps` interface so the
 same code runs on the GPU (DeviceOps: the C ABI + NCCL) and, in the CPU tests,
 with a numpy restatement of the chunk tree over gloo.
@@ -25,7 +30,7 @@ from typing import Protocol
 import numpy as np
 
 from . import _abi as A
-from .api import AdProblemSpec, Context, ParticleEstimate, _check, default_context
+from .api import AdProblemSpec, BvpProblemSpec, Context, ParticleEstimate, _check, default_context
 
 CHUNK = A.SMC_CHUNK
 
@@ -120,14 +125,14 @@ class DeviceOps:
         width = max(counts)
         on_host = dist.get_backend(self.group) == "gloo"
         dev = torch.device("cpu") if on_host else self.dev
-        buf = torch.zeros((self.n_obs, width), dtype=torch.float64, device=dev)
+        buf = torch.zeros((self.n_obs, width), dtype=local.dtype, device=dev)
         buf[:, : local.shape[1]] = local.to(dev)
         if on_host:
             parts = [torch.empty_like(buf) for _ in range(world)]
             dist.all_gather(parts, buf, group=self.group)
             gathered = torch.stack(parts)
         else:
-            gathered = torch.empty((world, self.n_obs, width), dtype=torch.float64, device=dev)
+            gathered = torch.empty((world, self.n_obs, width), dtype=local.dtype, device=dev)
             dist.all_gather_into_tensor(gathered, buf, group=self.group)
         return torch.cat([gathered[r, :, : counts[r]] for r in range(world)], dim=1).to(self.dev)
 
@@ -167,6 +172,67 @@ def observe_ad_emulated(spec: AdProblemSpec, seed: int, world: int, ctx: Context
         sq.append(ops.sq_partials(means, b, e).clone())
     sumsq = ops.finish(torch.cat(sq, dim=1))
     return estimates_from_sums(ops.to_host(sums), ops.to_host(sumsq), spec.n_particles)
+
+
+# ---------------------------------------------------------------------------
+# Dirichlet (BVP) walker sharding (single evaluation)
+# ---------------------------------------------------------------------------
+def walker_range(n_walkers: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous walker range of every observation for rank."""
+    return (n_walkers * rank) // world, (n_walkers * (rank + 1)) // world
+
+
+class BvpDeviceOps(DeviceOps):
+    """Walker sharding of observe_bvp: each rank runs its walker range of every
+    observation (smc_bvp_shard_values), the ranks all-gather the per-walker
+    results in walker order, and every rank reduces the whole set
+    (smc_bvp_reduce_values).  The reference compacts the valid walkers before
+    its tree (executor.cpp:93-101), so a walker's tree position depends on
+    failures anywhere before it: the exchange carries walker results (C3: 25 x
+    1e6 x 17 B over NVLink) rather than partial sums, and the estimates equal
+    observe_bvp bit for bit for any split."""
+
+    def __init__(self, spec: BvpProblemSpec, seed: int, ctx: Context | None = None, group=None):
+        super().__init__(spec, seed, ctx, group)
+
+    def shard(self, begin: int, end: int):
+        torch = self.torch
+        span = max(end - begin, 0)
+        vals = torch.empty((self.n_obs, span), dtype=torch.float64, device=self.dev)
+        aux = torch.empty_like(vals)
+        failed = torch.empty((self.n_obs, span), dtype=torch.uint8, device=self.dev)
+        _check(self.ctx.lib.smc_bvp_shard_values(self.ctx.handle, C.byref(self.pod), C.c_uint64(self.seed), begin,
+                                                 end, C.c_void_p(vals.data_ptr()), C.c_void_p(aux.data_ptr()),
+                                                 C.c_void_p(failed.data_ptr())))
+        return vals, aux, failed
+
+    def reduce(self, vals, aux, failed) -> list[ParticleEstimate]:
+        vals, aux, failed = vals.contiguous(), aux.contiguous(), failed.contiguous()
+        out = (A.smc_estimate * self.n_obs)()
+        _check(self.ctx.lib.smc_bvp_reduce_values(self.ctx.handle, C.c_void_p(vals.data_ptr()),
+                                                  C.c_void_p(aux.data_ptr()), C.c_void_p(failed.data_ptr()),
+                                                  vals.shape[1], self.n_obs, out))
+        return [ParticleEstimate._from(out[j]) for j in range(self.n_obs)]
+
+
+def observe_bvp_sharded(spec: BvpProblemSpec, seed: int, rank: int, world: int, ctx: Context | None = None,
+                        group=None) -> list[ParticleEstimate]:
+    """observe_bvp over `world` ranks by walker ranges (call on every rank)."""
+    ops = BvpDeviceOps(spec, seed, ctx, group)
+    n = spec.n_particles
+    counts = [walker_range(n, r, world)[1] - walker_range(n, r, world)[0] for r in range(world)]
+    b, e = walker_range(n, rank, world)
+    vals, aux, failed = ops.shard(b, e)
+    return ops.reduce(ops.all_gather(vals, counts), ops.all_gather(aux, counts), ops.all_gather(failed, counts))
+
+
+def observe_bvp_emulated(spec: BvpProblemSpec, seed: int, world: int, ctx: Context | None = None):
+    """The walker-sharded path with every rank's range run in turn on one GPU
+    and concatenated in rank order (what the all-gather delivers)."""
+    import torch
+    ops = BvpDeviceOps(spec, seed, ctx)
+    parts = [tuple(t.clone() for t in ops.shard(*walker_range(spec.n_particles, r, world))) for r in range(world)]
+    return ops.reduce(*(torch.cat([p[i] for p in parts], dim=1) for i in range(3)))
 
 
 def sample_range(n_samples: int, rank: int, world: int) -> tuple[int, int]:

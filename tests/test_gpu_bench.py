@@ -35,13 +35,14 @@ def test_bench_single_gpu_line():
     assert d["gpu_launches"] > 0
 
 
-def test_bench_two_ranks_plumbing():
+@pytest.mark.parametrize("config,parallel", [("c1", "particle-shard x2"), ("c3", "walker-shard x2")])
+def test_bench_two_ranks_plumbing(config, parallel):
     env = dict(os.environ, MASTER_ADDR="127.0.0.1")
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                         "--master-addr", "127.0.0.1", "--master-port", "29533", "bench.py", "--gpus", "2",
-                        "--config", "c1", "--steps", "3", "--warmup", "3", "--dist-backend", "gloo",
+                        "--config", config, "--steps", "3", "--warmup", "3", "--dist-backend", "gloo",
                         "--device", "0"], cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
     assert r.returncode == 0, r.stderr[-3000:]
     d = _last_json(r.stdout)
     assert d["n_gpus"] == 2 and d["value"] > 0
-    assert d["config"]["parallelism"].startswith("particle-shard x2")
+    assert d["config"]["parallelism"].startswith(parallel)

@@ -309,6 +309,26 @@ def test_more_observations_than_one_grid_dimension(ctx):
         assert one.mean == est[j].mean and one.std_error == est[j].std_error, j
 
 
+@pytest.mark.parametrize("max_steps", [10_000_000, 150])
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_bvp_walker_sharding_bit_identical(ctx, world, max_steps):
+    """SURVEY.md 8(e) for the Dirichlet map: walker ranges per rank, per-walker
+    results all-gathered in walker order, one reduction — equal to observe_bvp
+    bit for bit for any split, including runs where walkers fail (max_steps
+    150: the compaction before the reference's tree then depends on failures
+    in other ranks' ranges)."""
+    from paper_1808_10580_b200 import distributed as D
+    spec = specs.paper_bvp(n_particles=5000)
+    spec.max_steps = max_steps
+    want = S.observe_bvp(spec, 606, ctx=ctx)
+    got = D.observe_bvp_emulated(spec, 606, world, ctx=ctx)
+    if max_steps == 150:
+        assert sum(e.n_failed for e in want) > 0
+    for a, b in zip(got, want):
+        assert (a.mean, a.std_error, a.n_particles, a.n_failed, a.aux_mean) == \
+            (b.mean, b.std_error, b.n_particles, b.n_failed, b.aux_mean)
+
+
 # ---------------------------------------------------------------- FP32 -----
 def test_fp32_within_three_standard_errors(ctx, golden):
     spec = specs.c1_two_mode(n_particles=10000, precision=S.Precision.fp32)
