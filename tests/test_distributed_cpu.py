@@ -117,3 +117,45 @@ def test_chunk_ranges_partition():
             assert rs[0][0] == 0 and rs[-1][1] == n_chunks
             assert all(rs[i][1] == rs[i + 1][0] for i in range(world - 1))
             assert max(e - b for b, e in rs) - min(e - b for b, e in rs) <= 1
+
+
+def _gather_worker(rank, world, port, n, result_q):
+    """DeviceOps.all_gather over gloo with ragged walker ranges, float64 and
+    uint8 (the Dirichlet walker-sharding exchange): the rank-ordered result
+    must be the unsharded [n_obs][n] array."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ops = D.DeviceOps.__new__(D.DeviceOps)  # the exchange only: no device context
+        ops.torch, ops.n_obs, ops.dev, ops.group = torch, 4, torch.device("cpu"), None
+        full_v = torch.arange(4 * n, dtype=torch.float64).reshape(4, n) * 0.5
+        full_f = (torch.arange(4 * n).reshape(4, n) % 7 == 0).to(torch.uint8)
+        counts = [D.walker_range(n, r, world)[1] - D.walker_range(n, r, world)[0] for r in range(world)]
+        b, e = D.walker_range(n, rank, world)
+        gv = ops.all_gather(full_v[:, b:e].clone(), counts)
+        gf = ops.all_gather(full_f[:, b:e].clone(), counts)
+        result_q.put((rank, bool(torch.equal(gv, full_v)) and bool(torch.equal(gf, full_f)) and gf.dtype == torch.uint8))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 1001), (3, 10)])
+def test_walker_sharding_gather(world, n):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    prt = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, prt, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in results), results
+
+
+def test_walker_ranges_partition():
+    for n in (2, 7, 1000, 1_000_000):
+        for world in (1, 2, 3, 8):
+            rs = [D.walker_range(n, r, world) for r in range(world)]
+            assert rs[0][0] == 0 and rs[-1][1] == n
+            assert all(rs[i][1] == rs[i + 1][0] for i in range(world - 1))
