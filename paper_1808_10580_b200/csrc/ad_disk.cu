@@ -4,12 +4,13 @@
 // The lattice velocity with every loop bound known: the
 // powers P2[j] = e^{2 pi i j x2} and Q[j] = j P2[j] live in registers, each
 // row's +/-j pairs unroll into 8 DFMAs on 4 coefficients, and every row folds
-// into v through P1[k1] = e^{2 pi i k1 x1}.  Coefficients are staged once per
-// block in shared memory and read with broadcast vector loads at compile-time
-// offsets, each load feeding all P particles of the thread.  One coefficient
-// block per parameter sample (blockIdx.z), disk_shape.h layout.  Modes absent from
-// the caller's field are zero coefficients; the host only picks this kernel
-// when the field fills most of its disk.
+// into v through P1[k1] = e^{2 pi i k1 x1}.  Single-sample launches pass the
+// coefficient block as a kernel parameter (FP64: uniform-register operands;
+// FP32: packed FFMA2 form); batched launches stage one block per parameter
+// sample in shared memory and read it with broadcast vector loads at
+// compile-time offsets (grid order: launch_k).  disk_shape.h layout.  Modes
+// absent from the caller's field are zero coefficients; the host only picks
+// this kernel when the field fills most of its disk.
 #include <cuda_runtime.h>
 
 #include <cstdlib>

@@ -2,10 +2,12 @@
 // |k| <= K with every loop bound known at compile time:
 // P2[j] = e^{2 pi i j x2} and Q[j] = j P2[j] in registers, each row's +/-j
 // pairs unrolled into 8 DFMAs on 4 coefficients, every row folded into v
-// through P1[k1] = e^{2 pi i k1 x1}.  Coefficients come from a block staged
-// in shared memory (disk_shape.h layout), read with broadcast vector loads at
-// compile-time offsets.  Used by K1 (ad_disk.cu) and the Dirichlet walkers
-// (bvp_disk.cu).
+// through P1[k1] = e^{2 pi i k1 x1}.  The coefficient accessor is a template
+// parameter: a block staged in shared memory (SmemCoef, broadcast vector
+// loads at compile-time offsets), the kernel-parameter block read through
+// uniform registers (ParamCoef, FP64), or the packed FP32 block whose pair
+// updates are FFMA2s (PackedCoef).  Used by K1 (ad_disk.cu) and the Dirichlet
+// walkers (bvp_disk.cu).
 #pragma once
 
 #include <type_traits>
