@@ -146,19 +146,6 @@ struct IsPacked : std::false_type {};
 template <int K>
 struct IsPacked<PackedCoef<K>> : std::true_type {};
 
-__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
-    uint64_t r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-    return r;
-}
-__device__ __forceinline__ void f2_unpack(uint64_t v, float& lo, float& hi) {
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
-}
-// acc += c * (s, s)   (ptxas folds the broadcast into the FFMA2 operand)
-__device__ __forceinline__ void f2_fma_bcast(uint64_t& acc, uint64_t c, float s) {
-    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(c), "l"(f2_pack(s, s)));
-}
-
 struct NoDiskParam {};
 
 template <int K, class T, int P>

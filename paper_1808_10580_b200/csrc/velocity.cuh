@@ -13,6 +13,9 @@
 // recurrence, (k1,k2)-sorted mode loop, w = 2 Re(v e), v += w d.
 #pragma once
 
+#include <cstdint>
+#include <type_traits>
+
 #include "fastmath.cuh"
 #include "images.h"
 #include "smc_device.cuh"
@@ -52,6 +55,20 @@ template <class T, class CT>
 __device__ __forceinline__ void load2(const CT* p, T& a, T& b) {
     a = T(p[0]);
     b = T(p[1]);
+}
+
+// Packed two-lane FP32 helpers (sm_100a fma.rn.f32x2 -> SASS FFMA2).
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t v, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+// acc += c * (s, s)   (ptxas folds the broadcast into the FFMA2 operand)
+__device__ __forceinline__ void f2_fma_bcast(uint64_t& acc, uint64_t c, float s) {
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(c), "l"(f2_pack(s, s)));
 }
 
 // Generic tiled lattice evaluation (any K, any mode set).  `cf` points to one
@@ -100,18 +117,45 @@ __device__ __forceinline__ void velocity_lattice(const LatticeImg& L, const CT* 
             }
             T Ar = T(0), Ai = T(0), Br = T(0), Bi = T(0);
             if (t == 0) load2(cf + L.g0_off + 2 * k1, Ar, Ai);
+            if constexpr (std::is_same<T, float>::value && std::is_same<CT, float>::value) {
+                // FP32 from a float table: four FFMA2 per pair on the loaded
+                // coefficient pairs (ar, ai) and (br, bi) as they sit in the
+                // LDS.128 registers; the cross terms accumulate separately,
+                // D = sum (br, bi) pi and E = sum (ar, ai) qi, and fold in at
+                // the row end: A += (-D.y, D.x), B' += (-E.y, E.x)
+                uint64_t A = f2_pack(Ar, Ai), D = f2_pack(0.0f, 0.0f), B = D, E = D;
 #pragma unroll
-            for (int q = 0; q < kLatticeTile; ++q) {
-                T ar, ai, br, bi;
-                load4(c + 4 * q, ar, ai, br, bi);
-                Ar = fma(ar, pr[q], Ar);
-                Ai = fma(ai, pr[q], Ai);
-                Br = fma(br, qr[q], Br);
-                Bi = fma(bi, qr[q], Bi);
-                Ar = fma(bi, -pi[q], Ar);
-                Ai = fma(br, pi[q], Ai);
-                Br = fma(ai, -qi[q], Br);
-                Bi = fma(ar, qi[q], Bi);
+                for (int q = 0; q < kLatticeTile; ++q) {
+                    const float4 v = *reinterpret_cast<const float4*>(c + 4 * q);
+                    const uint64_t c01 = f2_pack(v.x, v.y), c23 = f2_pack(v.z, v.w);
+                    f2_fma_bcast(A, c01, pr[q]);
+                    f2_fma_bcast(D, c23, pi[q]);
+                    f2_fma_bcast(B, c23, qr[q]);
+                    f2_fma_bcast(E, c01, qi[q]);
+                }
+                float dr, di, er, ei;
+                f2_unpack(A, Ar, Ai);
+                f2_unpack(D, dr, di);
+                f2_unpack(B, Br, Bi);
+                f2_unpack(E, er, ei);
+                Ar -= di;
+                Ai += dr;
+                Br -= ei;
+                Bi += er;
+            } else {
+#pragma unroll
+                for (int q = 0; q < kLatticeTile; ++q) {
+                    T ar, ai, br, bi;
+                    load4(c + 4 * q, ar, ai, br, bi);
+                    Ar = fma(ar, pr[q], Ar);
+                    Ai = fma(ai, pr[q], Ai);
+                    Br = fma(br, qr[q], Br);
+                    Bi = fma(bi, qr[q], Bi);
+                    Ar = fma(bi, -pi[q], Ar);
+                    Ai = fma(br, pi[q], Ai);
+                    Br = fma(ai, -qi[q], Br);
+                    Bi = fma(ar, qi[q], Bi);
+                }
             }
             acc2 = fma(T(k1), fma(p1r, Ar, -p1i * Ai), acc2);
             acc1 = fma(-p1r, Br, fma(p1i, Bi, acc1));

@@ -373,6 +373,23 @@ def test_fp32_param_path_matches_batched_path(ctx, K):
         assert batched[0, j]["mean"] == e.mean and batched[0, j]["std_error"] == e.std_error, j
 
 
+@pytest.mark.parametrize("disable_disk", [False, True])
+def test_fp32_tiled_kernel_within_three_standard_errors(ctx, monkeypatch, disable_disk):
+    """The FP32 tiled lattice kernel (packed FFMA2 pair updates, K > 12 or
+    SMC_DISABLE_DISK) against the FP64 parity path on the same streams."""
+    if disable_disk:
+        monkeypatch.setenv("SMC_DISABLE_DISK", "1")
+    prior = S.PriorSpec(14 if not disable_disk else 6, 1.0, 2.5)
+    U = np.random.default_rng(3).normal(size=(2, prior.dimension())) * 0.5
+    b64 = S.observe_ad_batched(specs.c4_base(n_particles=4000), prior, U, 12, ctx=ctx)
+    b32 = S.observe_ad_batched(specs.c4_base(n_particles=4000, precision=S.Precision.fp32), prior, U, 12, ctx=ctx)
+    assert np.all(np.abs(b32["mean"] - b64["mean"]) <= 3.0 * b64["std_error"])
+    spec = specs.c4_base(n_particles=4000, precision=S.Precision.fp32)
+    spec.velocity = S.VelocityField.fourier(S.velocity_from_coefficients(prior, U[0]))
+    single = S.observe_ad(spec, 12, ctx=ctx)
+    assert all(abs(e.mean - m) <= 3.0 * se for e, m, se in zip(single, b64["mean"][0], b64["std_error"][0]))
+
+
 # ---------------------------------------------------------------- BVP ------
 def test_bvp_box_matches_reference(ctx, golden):
     g = golden["bvp_box"]
