@@ -28,15 +28,38 @@ constexpr int kBlock = 128;
 
 using namespace disk;
 
+// FP32 with one particle per thread stages the packed FFMA2 block
+// (PackedShape) — the same arithmetic as the kernel-parameter form, so batched
+// and single-sample FP32 results are identical; otherwise the compute-type
+// copy of the disk_shape.h block.
+template <int K, class T, int P>
+constexpr bool kPackedSmem = std::is_same<T, float>::value && P == 1;
+template <int K, class T, int P>
+constexpr int kStagedFloats = kPackedSmem<K, T, P> ? PackedShape<K>::n_padded : DiskShape<K>::n_coef;
+
+template <int K, class T, int P>
+__device__ __forceinline__ void stage_sample(T* dst, const double* src) {
+    if constexpr (kPackedSmem<K, T, P>) {
+        stage_packed<K>(dst, src, threadIdx.x, kBlock);
+    } else {
+        for (int i = threadIdx.x; i < DiskShape<K>::n_coef; i += kBlock) dst[i] = T(src[i]);
+    }
+}
+
+template <int K, class T, int P, class Body>
+__device__ __forceinline__ void with_smem_coef(const T* staged, Body&& body) {
+    const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(staged));
+    if constexpr (kPackedSmem<K, T, P>) body(PackedSmemCoef<K>{base});
+    else body(SmemCoef<T>{base});
+}
+
 template <int K, class T, int P, int MINB>
 __global__ void __launch_bounds__(kBlock, MINB) ad_particles_disk(const AdLaunch L, const double* coef) {
     // this sample's coefficient block -> shared memory (compute type)
-    __shared__ __align__(16) T staged[DiskShape<K>::n_coef];
+    __shared__ __align__(16) T staged[kStagedFloats<K, T, P>];
     const int sample = L.obs_major ? blockIdx.y : blockIdx.z;
-    const double* src = coef + static_cast<int64_t>(sample) * DiskShape<K>::n_coef;
-    for (int i = threadIdx.x; i < DiskShape<K>::n_coef; i += kBlock) staged[i] = T(src[i]);
+    stage_sample<K, T, P>(staged, coef + static_cast<int64_t>(sample) * DiskShape<K>::n_coef);
     __syncthreads();
-    const SmemCoef<T> C{static_cast<uint32_t>(__cvta_generic_to_shared(staged))};
     const int obs = __ldg(L.obs_order + (L.obs_major ? blockIdx.z : blockIdx.y));
     const int64_t span = L.p_end - L.p_begin;
     const int64_t base = static_cast<int64_t>(blockIdx.x) * kBlock * P + threadIdx.x;
@@ -44,10 +67,12 @@ __global__ void __launch_bounds__(kBlock, MINB) ad_particles_disk(const AdLaunch
     int64_t local[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) local[p] = base + static_cast<int64_t>(p) * kBlock;
-    ad_particles_p<T, P>(L, obs, sample, local, span,
-                         [&](const T (&x1)[P], const T (&x2)[P], T (&v1)[P], T (&v2)[P], int) {
-                             velocity_disk<K, T, P>(C, x1, x2, v1, v2);
-                         });
+    with_smem_coef<K, T, P>(staged, [&](const auto& C) {
+        ad_particles_p<T, P>(L, obs, sample, local, span,
+                             [&](const T (&x1)[P], const T (&x2)[P], T (&v1)[P], T (&v2)[P], int) {
+                                 velocity_disk<K, T, P>(C, x1, x2, v1, v2);
+                             });
+    });
 }
 
 // Observation-major batched launches with >= 64 particles per observation
@@ -58,28 +83,29 @@ __global__ void __launch_bounds__(kBlock, MINB) ad_particles_disk(const AdLaunch
 // within one sample when the particle count is a multiple of 32.
 template <int K, class T, int MINB>
 __global__ void __launch_bounds__(kBlock, MINB) ad_particles_disk_flat(const AdLaunch L, const double* coef) {
-    constexpr int NC = DiskShape<K>::n_coef;
+    constexpr int NC = DiskShape<K>::n_coef;   // doubles per sample in `coef`
+    constexpr int NS = kStagedFloats<K, T, 1>;  // staged elements per sample
     constexpr int kMaxSamples = 3;
-    __shared__ __align__(16) T staged[kMaxSamples * NC];
+    __shared__ __align__(16) T staged[kMaxSamples * NS];
     const int64_t span = L.p_end - L.p_begin;
     const int64_t total = span * L.n_samples;
     const int64_t flat0 = static_cast<int64_t>(blockIdx.x) * kBlock;
     const int s0 = static_cast<int>(flat0 / span);
     const int64_t last = (flat0 + kBlock < total ? flat0 + kBlock : total) - 1;
     const int ns = static_cast<int>(last / span) - s0 + 1;
-    const double* src = coef + static_cast<int64_t>(s0) * NC;  // sample blocks are contiguous
-    for (int i = threadIdx.x; i < ns * NC; i += kBlock) staged[i] = T(src[i]);
+    for (int q = 0; q < ns; ++q) stage_sample<K, T, 1>(staged + q * NS, coef + static_cast<int64_t>(s0 + q) * NC);
     __syncthreads();
     const int64_t flat = flat0 + threadIdx.x;
     if (flat >= total) return;
     const int sample = static_cast<int>(flat / span);
     int64_t local[1] = {flat - static_cast<int64_t>(sample) * span};
     const int obs = __ldg(L.obs_order + blockIdx.y);
-    const SmemCoef<T> C{static_cast<uint32_t>(__cvta_generic_to_shared(staged + (sample - s0) * NC))};
-    ad_particles_p<T, 1>(L, obs, sample, local, span,
-                         [&](const T (&x1)[1], const T (&x2)[1], T (&v1)[1], T (&v2)[1], int) {
-                             velocity_disk<K, T, 1>(C, x1, x2, v1, v2);
-                         });
+    with_smem_coef<K, T, 1>(staged + (sample - s0) * NS, [&](const auto& C) {
+        ad_particles_p<T, 1>(L, obs, sample, local, span,
+                             [&](const T (&x1)[1], const T (&x2)[1], T (&v1)[1], T (&v2)[1], int) {
+                                 velocity_disk<K, T, 1>(C, x1, x2, v1, v2);
+                             });
+    });
 }
 
 // Single-sample launches take the coefficient block as a KERNEL PARAMETER

@@ -141,10 +141,44 @@ struct PackedCoef {
         c3 = v.y;
     }
 };
+// The same packed block staged in shared memory (batched FP32 launches).
+template <int K>
+struct PackedSmemCoef {
+    uint32_t base;  // shared-memory address of this sample's packed block
+    template <int O>  // O: offset in the disk_shape.h layout (row0 / g0 only)
+    __device__ __forceinline__ void get2(float& a, float& b) const {
+        static_assert(O >= DiskShape<K>::row0_offset, "pairs use pair4");
+        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2+%3];"
+                     : "=f"(a), "=f"(b)
+                     : "r"(base), "n"((O + PackedShape<K>::shift) * 4));
+    }
+    template <int I>
+    __device__ __forceinline__ void pair4(uint64_t& c0, uint64_t& c1, uint64_t& c2, uint64_t& c3) const {
+        asm volatile("ld.shared.v2.u64 {%0, %1}, [%2+%3];" : "=l"(c0), "=l"(c1) : "r"(base), "n"(I * 32));
+        asm volatile("ld.shared.v2.u64 {%0, %1}, [%2+%3];" : "=l"(c2), "=l"(c3) : "r"(base), "n"(I * 32 + 16));
+    }
+};
+// Stage one sample's packed FP32 block (PackedShape layout) from its
+// disk_shape.h double block; all threads of the block cooperate.
+template <int K>
+__device__ __forceinline__ void stage_packed(float* dst, const double* src, int tid, int nthreads) {
+    for (int i = tid; i < DiskShape<K>::n_pairs; i += nthreads) {
+        const float ar = float(src[4 * i]), ai = float(src[4 * i + 1]), br = float(src[4 * i + 2]),
+                    bi = float(src[4 * i + 3]);
+        float4* q = reinterpret_cast<float4*>(dst + 8 * i);
+        q[0] = make_float4(ar, ai, br, bi);
+        q[1] = make_float4(-bi, br, -ai, ar);
+    }
+    for (int i = DiskShape<K>::row0_offset + tid; i < DiskShape<K>::n_coef; i += nthreads)
+        dst[i + PackedShape<K>::shift] = float(src[i]);
+}
+
 template <class CA>
 struct IsPacked : std::false_type {};
 template <int K>
 struct IsPacked<PackedCoef<K>> : std::true_type {};
+template <int K>
+struct IsPacked<PackedSmemCoef<K>> : std::true_type {};
 
 struct NoDiskParam {};
 
@@ -180,8 +214,8 @@ __device__ __forceinline__ void disk_pair(const CA& C, const Powers<K, T, P>& W,
     }
 }
 
-template <int K, int K1, int J, class W_t>
-__device__ __forceinline__ void disk_pair_packed(const PackedCoef<K>& C, const W_t& W, uint64_t& A, uint64_t& B) {
+template <int K, int K1, int J, class CA, class W_t>
+__device__ __forceinline__ void disk_pair_packed(const CA& C, const W_t& W, uint64_t& A, uint64_t& B) {
     uint64_t c0, c1, c2, c3;
     C.template pair4<DiskShape<K>::pair_offset(K1) + J - 1>(c0, c1, c2, c3);
     f2_fma_bcast(A, c0, W.pr[0][J]);
@@ -190,8 +224,8 @@ __device__ __forceinline__ void disk_pair_packed(const PackedCoef<K>& C, const W
     f2_fma_bcast(B, c3, W.qi[0][J]);
 }
 
-template <int K, int K1, class W_t, int... Js>
-__device__ __forceinline__ void disk_row_pairs_packed(const PackedCoef<K>& C, const W_t& W, uint64_t& A, uint64_t& B,
+template <int K, int K1, class CA, class W_t, int... Js>
+__device__ __forceinline__ void disk_row_pairs_packed(const CA& C, const W_t& W, uint64_t& A, uint64_t& B,
                                                       std::integer_sequence<int, Js...>) {
     (disk_pair_packed<K, K1, Js + 1>(C, W, A, B), ...);
 }
