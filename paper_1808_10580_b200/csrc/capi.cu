@@ -369,7 +369,7 @@ int smc_abi_version(void) { return SMC_ABI_VERSION; }
 const char* smc_last_error(void) { return g_err.c_str(); }
 
 smc_status smc_create(int device, smc_ctx** out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         *out = nullptr;
         int n = 0;
         CK(cudaGetDeviceCount(&n));
@@ -389,21 +389,16 @@ void smc_destroy(smc_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->own_stream) cudaStreamSynchronize(ctx->own_stream);
-    for (DevBuf* b : {&ctx->image, &ctx->values, &ctx->aux, &ctx->flags, &ctx->flags2, &ctx->scratch, &ctx->sums, &ctx->means,
-                      &ctx->sumsq, &ctx->sumaux, &ctx->est, &ctx->counts, &ctx->tmp_a, &ctx->tmp_b, &ctx->tmp_c})
-        b->release();
-    ctx->staging.release();
-    ctx->est_host.release();
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
-    delete ctx;
+    delete ctx;  // every DevBuf / PinnedBuf member frees itself (RAII)
 }
 
 void* smc_stream(smc_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
 
 smc_status smc_set_stream(smc_ctx* ctx, void* stream) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         CK(cudaSetDevice(ctx->device));
         CK(cudaStreamSynchronize(ctx->stream));
         ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
@@ -411,22 +406,22 @@ smc_status smc_set_stream(smc_ctx* ctx, void* stream) {
 }
 
 smc_status smc_ad_resolved_dt(const smc_ad_problem* p, double* out) {
-    return guarded([&] { *out = ad_resolved_dt(*p); });
+    return guarded(__func__, [&] { *out = ad_resolved_dt(*p); });
 }
 
 smc_status smc_bvp_resolved_dt(const smc_bvp_problem* p, double* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         const PreparedVelocity v = prepare_velocity(p->velocity);
         *out = bvp_resolved_dt(*p, v);
     });
 }
 
 smc_status smc_velocity_validate(const smc_velocity* v) {
-    return guarded([&] { (void)prepare_velocity(*v); });
+    return guarded(__func__, [&] { (void)prepare_velocity(*v); });
 }
 
 smc_status smc_ad_validate(const smc_ad_problem* p) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         (void)prepare_velocity(p->velocity);
         check_kappa(p->kappa);
         check_scalar(p->initial_condition);
@@ -435,7 +430,7 @@ smc_status smc_ad_validate(const smc_ad_problem* p) {
 }
 
 smc_status smc_bvp_validate(const smc_bvp_problem* p) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         (void)prepare_velocity(p->velocity);
         check_kappa(p->kappa);
         check_scalar(p->forcing);
@@ -457,7 +452,7 @@ int smc_struct_sizes(int64_t* out, int cap) {
 int64_t smc_num_chunks(int64_t n_particles) { return (n_particles + kChunk - 1) / kChunk; }
 
 smc_status smc_ad_observe(smc_ctx* ctx, const smc_ad_problem* p, uint64_t seed, smc_estimate* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         CK(cudaSetDevice(ctx->device));
         ad_observe_range(ctx, *p, seed, 0, p->n_obs, out);
     });
@@ -465,7 +460,7 @@ smc_status smc_ad_observe(smc_ctx* ctx, const smc_ad_problem* p, uint64_t seed, 
 
 smc_status smc_ad_observe_single(smc_ctx* ctx, const smc_ad_problem* p, uint64_t obs_index, uint64_t seed,
                                  smc_estimate* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         CK(cudaSetDevice(ctx->device));
         // observe_ad_single validates first, then range-checks (forward_ad.cpp:64-67).
         (void)prepare_velocity(p->velocity);
@@ -480,7 +475,7 @@ smc_status smc_ad_observe_single(smc_ctx* ctx, const smc_ad_problem* p, uint64_t
 
 smc_status smc_ad_shard_partials(smc_ctx* ctx, const smc_ad_problem* p, uint64_t seed, int64_t chunk_begin,
                                  int64_t chunk_end, double* partials_dev) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         CK(cudaSetDevice(ctx->device));
         const PreparedVelocity v = prepare_velocity(p->velocity);
         check_kappa(p->kappa);
@@ -517,7 +512,7 @@ smc_status smc_ad_shard_partials(smc_ctx* ctx, const smc_ad_problem* p, uint64_t
 
 smc_status smc_tree_finish(smc_ctx* ctx, const double* partials_dev, int64_t n_obs, int64_t n_chunks,
                            double* sums_dev) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         CK(cudaSetDevice(ctx->device));
         double* scratch = ctx->scratch.get<double>(static_cast<size_t>(2 * n_obs * std::max<int64_t>(1, n_chunks)));
         int launches = 0;
@@ -530,7 +525,7 @@ smc_status smc_tree_finish(smc_ctx* ctx, const double* partials_dev, int64_t n_o
 
 smc_status smc_ad_shard_sq_partials(smc_ctx* ctx, const double* means_dev, int64_t n_obs, int64_t chunk_begin,
                                     int64_t chunk_end, double* partials_dev) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         CK(cudaSetDevice(ctx->device));
         if (n_obs != ctx->shard_n_obs) raise(SMC_EINVAL, "smc_ad_shard_sq_partials: observation count mismatch");
         const int64_t nloc = chunk_end - chunk_begin;
@@ -546,7 +541,7 @@ smc_status smc_ad_shard_sq_partials(smc_ctx* ctx, const double* means_dev, int64
 
 smc_status smc_ad_particle_values(smc_ctx* ctx, const smc_ad_problem* p, uint64_t obs_index, uint64_t seed,
                                   int64_t n, double* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         CK(cudaSetDevice(ctx->device));
         const PreparedVelocity v = prepare_velocity(p->velocity);
         check_kappa(p->kappa);
@@ -564,7 +559,7 @@ smc_status smc_ad_particle_values(smc_ctx* ctx, const smc_ad_problem* p, uint64_
 }
 
 smc_status smc_philox_device(smc_ctx* ctx, int64_t n, const uint32_t* ctr, const uint32_t* key, uint32_t* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         CK(cudaSetDevice(ctx->device));
         uint32_t* dc = ctx->tmp_a.get<uint32_t>(static_cast<size_t>(4 * n));
         uint32_t* dk = ctx->tmp_b.get<uint32_t>(static_cast<size_t>(2 * n));
@@ -579,7 +574,7 @@ smc_status smc_philox_device(smc_ctx* ctx, int64_t n, const uint32_t* ctr, const
 
 smc_status smc_normal_pairs_device(smc_ctx* ctx, uint64_t seed, uint64_t obs, uint64_t particle, int64_t n_blocks,
                                    double* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         CK(cudaSetDevice(ctx->device));
         if (obs > 0xFFFFFFFFull || particle > 0xFFFFFFFFull)
             raise(SMC_EINVAL, "StreamKey: obs/particle index exceeds 32-bit stream space");
@@ -592,7 +587,7 @@ smc_status smc_normal_pairs_device(smc_ctx* ctx, uint64_t seed, uint64_t obs, ui
 }
 
 smc_status smc_last_stats(smc_ctx* ctx, smc_stats* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         *out = ctx->stats;
         out->total_launches = ctx->total_launches;
     });
@@ -624,11 +619,11 @@ double fma_peak(smc_ctx* ctx, double ms, bool fp64) {
 }  // namespace
 
 smc_status smc_fp32_peak(smc_ctx* ctx, double ms, double* tflops) {
-    return guarded([&] { *tflops = fma_peak(ctx, ms, false); });
+    return guarded(__func__, [&] { *tflops = fma_peak(ctx, ms, false); });
 }
 
 smc_status smc_fp64_peak(smc_ctx* ctx, double ms, double* tflops) {
-    return guarded([&] { *tflops = fma_peak(ctx, ms, true); });
+    return guarded(__func__, [&] { *tflops = fma_peak(ctx, ms, true); });
 }
 
 smc_status smc_bvp_observe(smc_ctx* ctx, const smc_bvp_problem* p, uint64_t seed, smc_estimate* out) {
@@ -678,7 +673,7 @@ static void reduce_bvp(smc_ctx* ctx, const double* values, const double* aux, co
 
 smc_status smc_bvp_observe_range(smc_ctx* ctx, const smc_bvp_problem* p, uint64_t seed, int64_t obs_begin,
                                  int64_t obs_count, smc_estimate* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (obs_begin < 0 || obs_count < 0 || obs_begin + obs_count > p->n_obs)
             raise(SMC_ERANGE, "observe_bvp: observation range out of bounds");
         CK(cudaSetDevice(ctx->device));
@@ -693,7 +688,7 @@ smc_status smc_bvp_observe_range(smc_ctx* ctx, const smc_bvp_problem* p, uint64_
 
 smc_status smc_bvp_shard_values(smc_ctx* ctx, const smc_bvp_problem* p, uint64_t seed, int64_t walker_begin,
                                 int64_t walker_end, double* values_dev, double* aux_dev, uint8_t* failed_dev) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (walker_begin < 0 || walker_end > p->n_particles || walker_begin > walker_end)
             raise(SMC_ERANGE, "smc_bvp_shard_values: walker range out of bounds");
         CK(cudaSetDevice(ctx->device));
@@ -721,7 +716,7 @@ smc_status smc_bvp_shard_values(smc_ctx* ctx, const smc_bvp_problem* p, uint64_t
 
 smc_status smc_bvp_reduce_values(smc_ctx* ctx, const double* values_dev, const double* aux_dev,
                                  const uint8_t* failed_dev, int64_t n_walkers, int64_t n_obs, smc_estimate* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (n_walkers < 2 || n_obs < 1)
             raise(SMC_EINVAL, "smc_bvp_reduce_values: need >= 2 walkers and >= 1 observation");
         CK(cudaSetDevice(ctx->device));
@@ -734,7 +729,7 @@ smc_status smc_bvp_reduce_values(smc_ctx* ctx, const double* values_dev, const d
 
 smc_status smc_bvp_forcing_basis(smc_ctx* ctx, const smc_bvp_problem* p, uint64_t seed, double* mean_bc,
                                  double* mean_basis, double* mean_tau, int64_t* n_failed) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         CK(cudaSetDevice(ctx->device));
         if (p->forcing.kind != SMC_SCALAR_BUMPS || p->forcing.n_terms < 1 || p->forcing.n_terms > 4)
             raise(SMC_EINVAL, "bvp_forcing_basis: forcing must be a sum of 1..4 Gaussian bumps");
@@ -763,8 +758,7 @@ smc_status smc_bvp_forcing_basis(smc_ctx* ctx, const smc_bvp_problem* p, uint64_
         const int64_t chunks = smc_num_chunks(n);
         double* cvals = ctx->tmp_a.get<double>(total);
         double* caux = ctx->tmp_b.get<double>(total);
-        DevBuf ctmp;
-        int64_t* chunk_tmp = ctmp.get<int64_t>(static_cast<size_t>(2 * n_obs * chunks));
+        int64_t* chunk_tmp = ctx->chunk_tmp.get<int64_t>(static_cast<size_t>(2 * n_obs * chunks));
         int64_t* counts = ctx->counts.get<int64_t>(static_cast<size_t>(n_obs));
         double* scratch = ctx->scratch.get<double>(static_cast<size_t>(2 * n_obs * std::max<int64_t>(chunks, 1)));
         double* sums = ctx->sums.get<double>(static_cast<size_t>(n_obs * (nb + 2)));
@@ -788,7 +782,6 @@ smc_status smc_bvp_forcing_basis(smc_ctx* ctx, const smc_bvp_problem* p, uint64_
         CK(cudaMemcpyAsync(hc.data(), counts, sizeof(int64_t) * n_obs, cudaMemcpyDeviceToHost, s));
         CK(cudaEventRecord(ctx->ev[2], s));
         CK(cudaStreamSynchronize(s));
-        ctmp.release();
         finish_stats(ctx);
         for (int64_t j = 0; j < n_obs; ++j) {
             if (hc[static_cast<size_t>(j)] == 0) raise(SMC_ERUNTIME, "map_reduce: every particle of an observation failed");
@@ -803,7 +796,7 @@ smc_status smc_bvp_forcing_basis(smc_ctx* ctx, const smc_bvp_problem* p, uint64_
 
 smc_status smc_bvp_particle_values(smc_ctx* ctx, const smc_bvp_problem* p, uint64_t obs_index, uint64_t seed,
                                    int64_t n, double* values, double* aux, uint8_t* failed) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         CK(cudaSetDevice(ctx->device));
         if (obs_index >= static_cast<uint64_t>(p->n_obs)) raise(SMC_ERANGE, "observation index out of range");
         BvpLaunch L = prepare_bvp(ctx, *p, static_cast<int64_t>(obs_index), 1);

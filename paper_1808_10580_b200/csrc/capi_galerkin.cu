@@ -31,7 +31,7 @@ int64_t smc_galerkin_n_basis(const smc_galerkin_basis* basis) {
 }
 
 smc_status smc_galerkin_modes(const smc_galerkin_basis* basis, int32_t* modes) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         const GalerkinModes m = galerkin_modes(*basis);
         for (int64_t i = 0; i < m.size(); ++i) {
             modes[2 * i] = m.k1[static_cast<size_t>(i)];
@@ -42,7 +42,7 @@ smc_status smc_galerkin_modes(const smc_galerkin_basis* basis, int32_t* modes) {
 
 smc_status smc_galerkin_spectral_radius(smc_ctx*, const smc_ad_problem* prob, const smc_galerkin_basis* basis,
                                         double* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         const PreparedVelocity v = galerkin_check_inputs(*prob);
         const GalerkinModes m = galerkin_modes(*basis);
         *out = galerkin_radius(galerkin_assemble(prob->kappa, v, m), m.size());
@@ -51,7 +51,7 @@ smc_status smc_galerkin_spectral_radius(smc_ctx*, const smc_ad_problem* prob, co
 
 smc_status smc_galerkin_solve_ad(smc_ctx* ctx, const smc_ad_problem* prob, const smc_galerkin_basis* basis,
                                  double dt_ref, smc_galerkin_result* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         CK(cudaSetDevice(ctx->device));
         const smc_ad_problem& p = *prob;
         const PreparedVelocity v = galerkin_check_inputs(p);
@@ -181,7 +181,7 @@ smc_status smc_galerkin_solve_ad(smc_ctx* ctx, const smc_ad_problem* prob, const
 
 smc_status smc_galerkin_field_grid(smc_ctx* ctx, const smc_galerkin_basis* basis, const double* coefficients,
                                    int32_t n, double* grid) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         CK(cudaSetDevice(ctx->device));
         if (n < 2) raise(SMC_EINVAL, "galerkin_field_grid: n must be >= 2");
         const GalerkinModes m = galerkin_modes(*basis);

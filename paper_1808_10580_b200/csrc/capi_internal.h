@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -33,8 +34,19 @@ extern thread_local std::string g_err;
                                                     " (" #x ")");                                   \
     } while (0)
 
+// Every C-ABI entry runs inside guarded(__func__, ...): one NVTX range named
+// after the entry point (visible in nsys / ncu --nvtx), exceptions mapped to
+// the smc_status of the reference's exception type.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 template <class F>
-smc_status guarded(F&& f) {
+smc_status guarded(const char* name, F&& f) {
+    NvtxRange range(name);
     try {
         f();
         return SMC_OK;
@@ -50,9 +62,16 @@ smc_status guarded(F&& f) {
     }
 }
 
+// Device / pinned buffers that grow on demand and are reused across calls.
+// RAII and non-copyable: a context's buffers are all released by its
+// destructor, so a new buffer cannot be forgotten in smc_destroy.
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
     template <class T>
     T* get(size_t n) {
         const size_t bytes = std::max<size_t>(n * sizeof(T), 16);
@@ -75,6 +94,10 @@ struct DevBuf {
 struct PinnedBuf {
     void* p = nullptr;
     size_t cap = 0;
+    PinnedBuf() = default;
+    PinnedBuf(const PinnedBuf&) = delete;
+    PinnedBuf& operator=(const PinnedBuf&) = delete;
+    ~PinnedBuf() { release(); }
     template <class T>
     T* get(size_t n) {
         const size_t bytes = std::max<size_t>(n * sizeof(T), 16);
@@ -128,6 +151,7 @@ struct smc_ctx {
     int64_t total_launches = 0;
     cudaEvent_t ev[4] = {};
     DevBuf image, values, aux, flags, flags2, scratch, sums, means, sumsq, sumaux, est, counts, tmp_a, tmp_b, tmp_c;
+    DevBuf chunk_tmp;  // compaction scan scratch of smc_bvp_forcing_basis
     DevBuf pk_ip, pk_im, pk_kp, pk_km, pk_ms, pk_u, pk_blocks, pk_bad;  // device u -> field packing
     DevBuf gal_A, gal_t0, gal_t1, gal_k1, gal_k2, gal_obs, gal_grid;  // Galerkin reference solver
     PinnedBuf staging, est_host;

@@ -11,7 +11,7 @@ extern "C" {
 smc_status smc_ad_observe_batched(smc_ctx* ctx, const smc_ad_problem* base, const smc_prior* prior,
                                   int64_t n_samples, const double* u, const uint64_t* seeds, uint64_t seed,
                                   smc_estimate* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         CK(cudaSetDevice(ctx->device));
         if (n_samples < 1) raise(SMC_EINVAL, "observe_ad_batched: need at least one sample");
         if (prior->cutoff <= 0) raise(SMC_EINVAL, "FourierVelocityField: max_wavenumber must be positive");
@@ -94,7 +94,7 @@ int64_t smc_pcn_num_samples(const smc_chain_config* cfg) {
 smc_status smc_pcn_chains(smc_ctx* ctx, const smc_ad_problem* forward, const smc_prior* prior, const double* data,
                           double noise_std, uint64_t forward_seed, int64_t n_chains, const uint64_t* chain_seeds,
                           const double* u0, const smc_chain_config* cfg, smc_chain_outputs* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         CK(cudaSetDevice(ctx->device));
         // run_chain's checks (inference.cpp:172-173), prior_draw/chain_init's
         // (inference.cpp:17-21, :89-91, :125-133), pcn_step's (:138).

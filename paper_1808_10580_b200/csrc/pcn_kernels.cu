@@ -113,11 +113,11 @@ __global__ void pcn_propose_kernel(PcnStep S) {
 // disk_fill, uncontracted (this TU is -fmad=false), so the blocks equal the
 // host-filled ones bit for bit.  A non-finite coefficient raises *bad (the
 // FourierVelocityField ctor check, fields.cpp:46-47).
-__global__ void pcn_pack_kernel(PackDev M, const double* __restrict__ Up, int64_t dim, double* __restrict__ blocks,
-                                int* bad) {
+__global__ void pcn_pack_kernel(PackDev M, const double* __restrict__ Up, int64_t dim, int64_t n_samples,
+                                double* __restrict__ blocks, int* bad) {
     const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t b = blockIdx.y;
     if (q >= M.stride) return;
+    for (int64_t b = blockIdx.y; b < n_samples; b += gridDim.y) {  // gridDim.y <= 65535
     const double* u = Up + b * dim;
     const int32_t a = M.ip[q], c = M.im[q];
     const int ms = M.ms[q];
@@ -137,6 +137,7 @@ __global__ void pcn_pack_kernel(PackDev M, const double* __restrict__ Up, int64_
         v = ms > 0 ? v + g : v - g;
     }
     blocks[b * M.stride + q] = v;
+    }
 }
 
 // misfit (inference.cpp:98-103), the chain's uniform, the accept rule
@@ -178,13 +179,14 @@ __global__ void pcn_accept_kernel(PcnStep S, const smc_estimate* __restrict__ es
 
 __global__ void pcn_commit_kernel(PcnStep S) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t b = blockIdx.y;
     if (i >= S.dim) return;
-    double* U = S.U + b * S.dim;
     const int64_t slot = step_fields(S).sample_slot;
-    if (S.acc_flag[b]) U[i] = S.Up[b * S.dim + i];
-    if (S.map_flag[b]) S.map_u[b * S.dim + i] = U[i];
-    if (slot >= 0 && S.samples) S.samples[(b * S.n_samples + slot) * S.dim + i] = U[i];
+    for (int64_t b = blockIdx.y; b < S.n_chains; b += gridDim.y) {  // gridDim.y <= 65535
+        double* U = S.U + b * S.dim;
+        if (S.acc_flag[b]) U[i] = S.Up[b * S.dim + i];
+        if (S.map_flag[b]) S.map_u[b * S.dim + i] = U[i];
+        if (slot >= 0 && S.samples) S.samples[(b * S.n_samples + slot) * S.dim + i] = U[i];
+    }
 }
 
 __global__ void pcn_advance_kernel(int64_t* it) { *it += 1; }
@@ -198,8 +200,9 @@ cudaError_t launch_pcn_propose(const PcnStep& S, cudaStream_t s) {
 
 cudaError_t launch_pack(const PackDev& M, const double* Up, int64_t dim, int64_t n_samples, double* blocks, int* bad,
                         cudaStream_t s) {
-    const dim3 grid(static_cast<unsigned>((M.stride + 255) / 256), static_cast<unsigned>(n_samples));
-    pcn_pack_kernel<<<grid, 256, 0, s>>>(M, Up, dim, blocks, bad);
+    const dim3 grid(static_cast<unsigned>((M.stride + 255) / 256),
+                    static_cast<unsigned>(n_samples < 65535 ? n_samples : 65535));
+    pcn_pack_kernel<<<grid, 256, 0, s>>>(M, Up, dim, n_samples, blocks, bad);
     return cudaGetLastError();
 }
 
@@ -215,7 +218,8 @@ cudaError_t launch_pcn_advance(int64_t* it_dev, cudaStream_t s) {
 }
 
 cudaError_t launch_pcn_commit(const PcnStep& S, cudaStream_t s) {
-    const dim3 grid(static_cast<unsigned>((S.dim + 255) / 256), static_cast<unsigned>(S.n_chains));
+    const dim3 grid(static_cast<unsigned>((S.dim + 255) / 256),
+                    static_cast<unsigned>(S.n_chains < 65535 ? S.n_chains : 65535));
     pcn_commit_kernel<<<grid, 256, 0, s>>>(S);
     return cudaGetLastError();
 }

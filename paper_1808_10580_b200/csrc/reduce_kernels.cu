@@ -13,6 +13,8 @@
 // bits as one device would produce.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "kernels.h"
 #include "../../include/scalarmc_b200.h"
 
@@ -167,14 +169,23 @@ __global__ void __launch_bounds__(kThreads) compact_kernel(const double* __restr
 
 }  // namespace
 
+// Segments index gridDim.y (<= 65535): larger segment counts run as several
+// launches over pointer-offset segment groups (results unchanged).
+constexpr int64_t kMaxGridY = 65535;
+
 cudaError_t launch_tree_pass(const double* in, int64_t in_stride, const int64_t* counts, int64_t n_uniform,
                              int64_t n_seg, double* out, int64_t out_stride, const double* center, int mode,
                              cudaStream_t s) {
     // n_uniform is the max count when counts is given.
     const int64_t chunks = (n_uniform + kChunk - 1) / kChunk;
     if (chunks <= 0 || n_seg <= 0) return cudaSuccess;
-    const dim3 grid(static_cast<unsigned>(chunks), static_cast<unsigned>(n_seg));
-    tree_pass_kernel<<<grid, kThreads, 0, s>>>(in, in_stride, counts, n_uniform, out, out_stride, center, mode);
+    for (int64_t g = 0; g < n_seg; g += kMaxGridY) {
+        const int64_t ng = std::min(kMaxGridY, n_seg - g);
+        const dim3 grid(static_cast<unsigned>(chunks), static_cast<unsigned>(ng));
+        tree_pass_kernel<<<grid, kThreads, 0, s>>>(in + g * in_stride, in_stride, counts ? counts + g : nullptr,
+                                                   n_uniform, out + g * out_stride, out_stride,
+                                                   center ? center + g : nullptr, mode);
+    }
     return cudaGetLastError();
 }
 
@@ -231,11 +242,19 @@ cudaError_t compact_valid(const double* values, const double* aux, const uint8_t
     if (chunks <= 0 || n_seg <= 0) return cudaSuccess;
     int64_t* chunk_counts = chunk_tmp;
     int64_t* chunk_offsets = chunk_tmp + n_seg * chunks;
-    const dim3 grid(static_cast<unsigned>(chunks), static_cast<unsigned>(n_seg));
-    count_valid_kernel<<<grid, kThreads, 0, s>>>(failed, n, chunks, chunk_counts);
+    for (int64_t g = 0; g < n_seg; g += kMaxGridY) {
+        const int64_t ng = std::min(kMaxGridY, n_seg - g);
+        const dim3 grid(static_cast<unsigned>(chunks), static_cast<unsigned>(ng));
+        count_valid_kernel<<<grid, kThreads, 0, s>>>(failed + g * n, n, chunks, chunk_counts + g * chunks);
+    }
     scan_chunks_kernel<<<static_cast<unsigned>((n_seg + 63) / 64), 64, 0, s>>>(chunk_counts, chunks, n_seg,
                                                                               chunk_offsets, counts);
-    compact_kernel<<<grid, kThreads, 0, s>>>(values, aux, failed, n, chunks, chunk_offsets, cvalues, caux);
+    for (int64_t g = 0; g < n_seg; g += kMaxGridY) {
+        const int64_t ng = std::min(kMaxGridY, n_seg - g);
+        const dim3 grid(static_cast<unsigned>(chunks), static_cast<unsigned>(ng));
+        compact_kernel<<<grid, kThreads, 0, s>>>(values + g * n, aux + g * n, failed + g * n, n, chunks,
+                                                 chunk_offsets + g * chunks, cvalues + g * n, caux + g * n);
+    }
     return cudaGetLastError();
 }
 
