@@ -162,6 +162,45 @@ void smc_destroy(smc_ctx* ctx);
 const char* smc_last_error(void);
 int smc_abi_version(void);
 
+/* ---- multi-device contexts ------------------------------
+ * A context over several GPUs of one box.  smc_ad_observe, smc_ad_observe_single,
+ * smc_bvp_observe(_range), smc_ad_observe_batched and smc_pcn_chains on it shard
+ * their work over the GPUs (particle chunks / walker ranges / parameter samples /
+ * chains) and combine ranks with a small deterministic NCCL exchange over
+ * NVLink, so the estimates are bit-identical to one GPU for any device count;
+ * every other call runs on the first device.  The reference's parallelism knob
+ * is `workers` (executor.cpp:45-85); here it is the device list.
+ *
+ * One process, several GPUs: smc_create_multi(ndev, devs) (ncclCommInitAll).
+ * A list that repeats a device is allowed (NCCL is then replaced by peer copies
+ * ordered by events — the same arithmetic, used to test sharding on one GPU).
+ * One process per GPU (torchrun): rank 0 calls smc_nccl_unique_id, the caller
+ * broadcasts the 128 bytes (e.g. torch.distributed), and every rank calls
+ * smc_create_rank(device, rank, world, id) — collective, like ncclCommInitRank.
+ * Every rank then calls the forward maps with the same arguments and receives
+ * the full result. */
+#define SMC_UNIQUE_ID_BYTES 128
+smc_status smc_nccl_unique_id(uint8_t* out /* [SMC_UNIQUE_ID_BYTES] */);
+smc_status smc_create_multi(int ndev, const int* devs, smc_ctx** out);
+smc_status smc_create_rank(int device, int rank, int world, const uint8_t* unique_id, smc_ctx** out);
+/* Host-staged variant for ranks that cannot share an NCCL communicator (e.g.
+ * several ranks on one GPU when testing the plumbing): at every exchange the
+ * library writes this rank's contribution to buf[displ[rank], +bytes[rank]) and
+ * calls exchange(user, buf, displ, bytes, world), which must fill the other
+ * ranks' slices (an all-gather over the caller's transport, e.g.
+ * torch.distributed over gloo) and return 0. */
+typedef int (*smc_exchange_fn)(void* user, uint8_t* buf, const uint64_t* displ, const uint64_t* bytes, int world);
+smc_status smc_create_rank_hosted(int device, int rank, int world, smc_exchange_fn exchange, void* user,
+                                  smc_ctx** out);
+typedef struct smc_group_desc {
+    int32_t world;      /* ranks the forward maps are sharded over */
+    int32_t rank;       /* rank of this context's first device */
+    int32_t n_local;    /* devices driven by this process */
+    int32_t nccl;       /* 1: NCCL exchange, 0: single device or emulated exchange */
+    int32_t devices[8]; /* first 8 local devices (-1 unused) */
+} smc_group_desc;
+smc_status smc_group_query(smc_ctx* ctx, smc_group_desc* out);
+
 /* ---- forward maps (the drop-in boundary) --------------------------------- */
 
 /* observe_ad (include/scalarmc/forward_ad.hpp:39-40, src/forward_ad.cpp:53-60).
@@ -195,23 +234,6 @@ smc_status smc_bvp_observe(smc_ctx* ctx, const smc_bvp_problem* prob, uint64_t s
  * out: [obs_count]. */
 smc_status smc_bvp_observe_range(smc_ctx* ctx, const smc_bvp_problem* prob, uint64_t seed, int64_t obs_begin,
                                  int64_t obs_count, smc_estimate* out);
-
-/* Walker sharding of one Dirichlet evaluation: run walkers
- * [walker_begin, walker_end) of every observation (their own stream keys, so
- * the results do not depend on the split) and write the per-walker results
- * to caller-owned DEVICE arrays [n_obs][walker_end - walker_begin]: value
- * (theta_bc(X_tau) - int f), exit time, failed flag.  The ranks then
- * all-gather the arrays (rank order = walker order) and reduce the whole
- * [n_obs][n_particles] set with smc_bvp_reduce_values, which reproduces
- * observe_bvp bit for bit for any split: the reference's compaction of valid
- * walkers depends on failures anywhere before a walker, so the exchange
- * carries walker results rather than partial sums. */
-smc_status smc_bvp_shard_values(smc_ctx* ctx, const smc_bvp_problem* prob, uint64_t seed, int64_t walker_begin,
-                                int64_t walker_end, double* values_dev, double* aux_dev, uint8_t* failed_dev);
-/* reduce_observation (executor.cpp:87-117) of device arrays
- * [n_obs][n_walkers]; out: [n_obs] on the host. */
-smc_status smc_bvp_reduce_values(smc_ctx* ctx, const double* values_dev, const double* aux_dev,
-                                 const uint8_t* failed_dev, int64_t n_walkers, int64_t n_obs, smc_estimate* out);
 
 /* Forcing basis of the Dirichlet map.  With common
  * random numbers the walker paths do not depend on the forcing amplitudes F,
@@ -314,33 +336,14 @@ smc_status smc_velocity_validate(const smc_velocity* v);
  * check their layout.  Returns the number written. */
 int smc_struct_sizes(int64_t* out, int cap);
 
-/* ---- sharded / device-level API (multi-GPU, one process per GPU) ----------
- * A forward map sharded over W ranks: particles of every observation are cut
- * into aligned chunks of SMC_CHUNK particles; rank r simulates chunks
- * [r*C/W, (r+1)*C/W).  Each rank produces exact aligned-tree partial sums per
- * chunk (the reference's pairwise_sum tree restricted to the chunk,
- * executor.cpp:11-26), the caller all-gathers them (NCCL), and every rank
- * finishes the same tree — so the result is bit-identical for any W. */
+/* ---- chunking -------------------------------------------------------------
+ * The reduction tree's leaf block: sharded forward maps split each
+ * observation's particles into chunks of SMC_CHUNK (executor.cpp:11-26 tree
+ * aligned at 1024 leaves). */
 #define SMC_CHUNK 1024
 
 /* Number of chunks per observation for n_particles. */
 int64_t smc_num_chunks(int64_t n_particles);
-
-/* Simulate this rank's chunk range of every observation, then write the
- * per-chunk value partials. partials_dev: device pointer [n_obs][n_chunks_local].
- * The per-particle values stay in the context for smc_ad_shard_sq_partials. */
-smc_status smc_ad_shard_partials(smc_ctx* ctx, const smc_ad_problem* prob, uint64_t seed,
-                                 int64_t chunk_begin, int64_t chunk_end, double* partials_dev);
-
-/* Finish the tree over all chunks: partials_dev [n_obs][n_chunks] (device) ->
- * sums_dev [n_obs] (device). */
-smc_status smc_tree_finish(smc_ctx* ctx, const double* partials_dev, int64_t n_obs,
-                           int64_t n_chunks, double* sums_dev);
-
-/* Second pass: chunk partials of (v - mean_j)^2 for the same chunk range.
- * means_dev: [n_obs] device. */
-smc_status smc_ad_shard_sq_partials(smc_ctx* ctx, const double* means_dev, int64_t n_obs,
-                                    int64_t chunk_begin, int64_t chunk_end, double* partials_dev);
 
 /* Device stream the context launches on (cudaStream_t as void*).  A caller
  * that already owns a stream (torch, NCCL) can hand it to the context so the

@@ -32,6 +32,7 @@ from .api import (  # noqa: F401
     ad_particle_values,
     bvp_particle_values,
     default_context,
+    nccl_unique_id,
     forcing_basis,
     GalerkinBasis,
     GalerkinResult,

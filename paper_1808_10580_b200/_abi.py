@@ -90,6 +90,17 @@ class smc_stats(C.Structure):
                 ("total_launches", C.c_int64)]
 
 
+class smc_group_desc(C.Structure):
+    _fields_ = [("world", C.c_int32), ("rank", C.c_int32), ("n_local", C.c_int32), ("nccl", C.c_int32),
+                ("devices", C.c_int32 * 8)]
+
+
+SMC_UNIQUE_ID_BYTES = 128
+# int (*)(void* user, uint8_t* buf, const uint64_t* displ, const uint64_t* bytes, int world)
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_uint8), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                          C.c_int)
+
+
 def dptr(a: np.ndarray | None):
     if a is None:
         return _dp()
@@ -109,6 +120,11 @@ def iptr(a: np.ndarray | None):
 _PROTOS = {
     "smc_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
     "smc_destroy": (None, [C.c_void_p]),
+    "smc_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+    "smc_create_multi": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_void_p)]),
+    "smc_create_rank": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_uint8), C.POINTER(C.c_void_p)]),
+    "smc_group_query": (C.c_int, [C.c_void_p, C.POINTER(smc_group_desc)]),
+    "smc_create_rank_hosted": (C.c_int, [C.c_int, C.c_int, C.c_int, EXCHANGE_FN, C.c_void_p, C.POINTER(C.c_void_p)]),
     "smc_last_error": (C.c_char_p, []),
     "smc_abi_version": (C.c_int, []),
     "smc_ad_observe": (C.c_int, [C.c_void_p, C.POINTER(smc_ad_problem), C.c_uint64,
@@ -123,10 +139,6 @@ _PROTOS = {
                                   C.POINTER(smc_estimate)]),
     "smc_bvp_observe_range": (C.c_int, [C.c_void_p, C.POINTER(smc_bvp_problem), C.c_uint64, C.c_int64,
                                         C.c_int64, C.POINTER(smc_estimate)]),
-    "smc_bvp_shard_values": (C.c_int, [C.c_void_p, C.POINTER(smc_bvp_problem), C.c_uint64, C.c_int64, C.c_int64,
-                                       C.c_void_p, C.c_void_p, C.c_void_p]),
-    "smc_bvp_reduce_values": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
-                                        C.POINTER(smc_estimate)]),
     "smc_bvp_forcing_basis": (C.c_int, [C.c_void_p, C.POINTER(smc_bvp_problem), C.c_uint64, _dp, _dp, _dp,
                                         C.POINTER(C.c_int64)]),
     "smc_pcn_num_samples": (C.c_int64, [C.POINTER(smc_chain_config)]),
@@ -146,11 +158,6 @@ _PROTOS = {
     "smc_bvp_validate": (C.c_int, [C.POINTER(smc_bvp_problem)]),
     "smc_velocity_validate": (C.c_int, [C.POINTER(smc_velocity)]),
     "smc_num_chunks": (C.c_int64, [C.c_int64]),
-    "smc_ad_shard_partials": (C.c_int, [C.c_void_p, C.POINTER(smc_ad_problem), C.c_uint64,
-                                        C.c_int64, C.c_int64, C.c_void_p]),
-    "smc_tree_finish": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p]),
-    "smc_ad_shard_sq_partials": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
-                                           C.c_int64, C.c_void_p]),
     "smc_stream": (C.c_void_p, [C.c_void_p]),
     "smc_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "smc_ad_particle_values": (C.c_int, [C.c_void_p, C.POINTER(smc_ad_problem), C.c_uint64,

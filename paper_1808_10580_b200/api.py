@@ -451,16 +451,47 @@ def _check(status: int) -> None:
 
 
 class Context:
-    """One CUDA device context (stream + persistent buffers), smc_ctx."""
+    """A device context (stream + persistent buffers), smc_ctx.
 
-    def __init__(self, device: int | None = None):
-        if device is None:
-            device = int(os.environ.get("LOCAL_RANK", "0"))
-        self.device = device
+    Context(device): one GPU.  Context(devices=[0, 1, ...]): one process
+    driving several GPUs (smc_create_multi); the forward maps then shard over
+    them and return the same bits as one GPU.  Context.for_rank(...): one GPU
+    of a one-process-per-GPU group (smc_create_rank; see
+    distributed.rank_context for the torch.distributed plumbing)."""
+
+    def __init__(self, device: int | None = None, *, devices: Sequence[int] | None = None):
         self.lib = A.load_library()
         h = C.c_void_p()
-        _check(self.lib.smc_create(device, C.byref(h)))
+        if devices is not None:
+            devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+            _check(self.lib.smc_create_multi(len(devices), devs, C.byref(h)))
+            device = int(devices[0])
+        else:
+            if device is None:
+                device = int(os.environ.get("LOCAL_RANK", "0"))
+            _check(self.lib.smc_create(device, C.byref(h)))
+        self.device = device
         self.handle = h
+
+    @classmethod
+    def for_rank(cls, device: int, rank: int, world: int, unique_id: bytes) -> "Context":
+        """Collective over the `world` ranks (ncclCommInitRank): every rank
+        calls it with the unique id rank 0 got from nccl_unique_id()."""
+        self = cls.__new__(cls)
+        self.lib = A.load_library()
+        h = C.c_void_p()
+        uid = (C.c_uint8 * A.SMC_UNIQUE_ID_BYTES).from_buffer_copy(bytes(unique_id))
+        _check(self.lib.smc_create_rank(int(device), int(rank), int(world), uid, C.byref(h)))
+        self.device = int(device)
+        self.handle = h
+        return self
+
+    def group(self) -> dict:
+        """World size, this context's rank, local devices and exchange kind."""
+        g = A.smc_group_desc()
+        _check(self.lib.smc_group_query(self.handle, C.byref(g)))
+        return {"world": g.world, "rank": g.rank, "n_local": g.n_local, "nccl": bool(g.nccl),
+                "devices": [d for d in g.devices if d >= 0]}
 
     def close(self):
         if self.handle:
@@ -491,6 +522,13 @@ class Context:
         out = C.c_double()
         _check(self.lib.smc_fp32_peak(self.handle, ms, C.byref(out)))
         return out.value
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId (rank 0 of a smc_create_rank group)."""
+    buf = (C.c_uint8 * A.SMC_UNIQUE_ID_BYTES)()
+    _check(A.load_library().smc_nccl_unique_id(buf))
+    return bytes(buf)
 
 
 _contexts: dict[int, Context] = {}

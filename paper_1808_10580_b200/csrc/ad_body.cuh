@@ -9,6 +9,7 @@
 // the velocity evaluator loads each coefficient once for all P particles.
 #pragma once
 
+#include "ad_unit.cuh"
 #include "kernels.h"
 #include "scalar_eval.cuh"
 #include "smc_device.cuh"
@@ -82,7 +83,7 @@ __device__ __forceinline__ void ad_particles_p(const AdLaunch& L, int obs, int s
             x2[p] -= floor(x2[p]);
         }
     }
-    double* out = L.values + (static_cast<int64_t>(sample) * L.n_obs + obs) * span;
+    double* out = ad_out_row(L, sample, obs, span);
 #pragma unroll
     for (int p = 0; p < P; ++p)
         if (local[p] < span) out[local[p]] = scalar_eval(L.theta0, double(x1[p]), double(x2[p]));

@@ -130,11 +130,15 @@ struct ParamBlock<K, float> {
 template <int K, class T, int MINB>
 __global__ void __launch_bounds__(kBlock, MINB)
     ad_particles_disk_param(const AdLaunch L, const typename ParamBlock<K, T>::type P) {
-    const int obs = blockIdx.y;
-    const int64_t span = L.p_end - L.p_begin;
+    int obs = blockIdx.y;
+    int64_t span = L.p_end - L.p_begin;
     const int64_t base = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x;
     if (base >= span) return;
     int64_t local[1] = {base};
+    if (L.unit_cpo > 0) {  // sharded launch (kernels.h unit mode)
+        if (!unit_coords(L, base, obs, local[0])) return;
+        span = L.n_particles;
+    }
     auto vel = [&](const T (&x1)[1], const T (&x2)[1], T (&v1)[1], T (&v2)[1], int zero) {
                              if constexpr (std::is_same<T, float>::value) {
                                  const PackedCoef<K> C{P};
@@ -171,7 +175,8 @@ cudaError_t launch_param(const AdLaunch& L, cudaStream_t s) {
         for (int i = PackedShape<K>::n_coef; i < PackedShape<K>::n_padded; ++i) dst[i] = 0.0f;
     }
     const int64_t span = L.p_end - L.p_begin;
-    const dim3 grid(static_cast<unsigned>((span + kBlock - 1) / kBlock), static_cast<unsigned>(L.n_obs), 1);
+    const dim3 grid(static_cast<unsigned>((span + kBlock - 1) / kBlock),
+                    static_cast<unsigned>(L.unit_cpo > 0 ? 1 : L.n_obs), 1);
     AdLaunch LK = L;
     LK.rk = make_round_keys(L.seed);
     ad_particles_disk_param<K, T, (K <= 8 ? 4 : 3)><<<grid, kBlock, 0, s>>>(LK, P);
@@ -261,10 +266,12 @@ cudaError_t dispatch(const AdLaunch& L, int K, const double* c, cudaStream_t s) 
 
 cudaError_t launch_ad_disk(const AdLaunch& L, int K, const double* coef, cudaStream_t s) {
     if (L.p_end - L.p_begin <= 0) return cudaSuccess;
+    // unit mode is single-sample with a host block: the kernel-parameter path only
+    if (L.unit_cpo > 0 && (L.n_samples != 1 || !L.host_disk || L.seeds)) return cudaErrorInvalidValue;
     // one coefficient block with its host copy: the kernel-parameter path
     // (SMC_DISK_P=2 keeps the shared-memory kernel, which has the P=2 form)
     const char* pe = std::getenv("SMC_DISK_P");
-    if (L.n_samples == 1 && L.host_disk && !L.seeds && !(pe && std::atoi(pe) == 2))
+    if (L.n_samples == 1 && L.host_disk && !L.seeds && (L.unit_cpo > 0 || !(pe && std::atoi(pe) == 2)))
         return L.precision == 1 ? dispatch_param<float>(L, K, s) : dispatch_param<double>(L, K, s);
     return L.precision == 1 ? dispatch<float>(L, K, coef, s) : dispatch<double>(L, K, coef, s);
 }

@@ -40,11 +40,16 @@ __global__ void __launch_bounds__(kBlock, 512 / kBlock) ad_particles(const AdLau
             __syncthreads();
         }
     }
-    const int64_t local = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x;
-    const int64_t span = L.p_end - L.p_begin;
+    int64_t local = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x;
+    int64_t span = L.p_end - L.p_begin;
     if (local >= span) return;
+    int ob = obs;
+    if (L.unit_cpo > 0) {  // sharded launch (kernels.h unit mode)
+        if (!unit_coords(L, local, ob, local)) return;
+        span = L.n_particles;
+    }
     const T c1 = T(L.vel.c1), c2 = T(L.vel.c2);
-    ad_particle<T>(L, obs, sample, local, span, [&](T x1, T x2, T& v1, T& v2) {
+    ad_particle<T>(L, ob, sample, local, span, [&](T x1, T x2, T& v1, T& v2) {
         if (is_const) {
             v1 = c1;
             v2 = c2;
@@ -60,7 +65,7 @@ template <class T, bool SMEM, int BS, bool OM>
 void go_om(const AdLaunch& L, int64_t nb, size_t smem, cudaStream_t s) {
     const dim3 grid = OM ? dim3(static_cast<unsigned>(nb), static_cast<unsigned>(L.n_samples),
                                 static_cast<unsigned>(L.n_obs))
-                         : dim3(static_cast<unsigned>(nb), static_cast<unsigned>(L.n_obs),
+                         : dim3(static_cast<unsigned>(nb), static_cast<unsigned>(L.unit_cpo > 0 ? 1 : L.n_obs),
                                 static_cast<unsigned>(L.n_samples));
     if constexpr (SMEM) {
         // once per instantiation and device (the attribute is per device)

@@ -13,6 +13,7 @@
 #define SMC_STRICT_TU 1
 #include <cuda_runtime.h>
 
+#include "ad_unit.cuh"
 #include "kernels.h"
 #include "scalar_eval.cuh"
 #include "smc_device.cuh"
@@ -25,10 +26,14 @@ constexpr int kBlock = 128;
 
 template <int KCAP>
 __global__ void __launch_bounds__(kBlock) ad_particles_strict(const AdLaunch L) {
-    const int obs = blockIdx.y;
-    const int64_t local = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x;
-    const int64_t span = L.p_end - L.p_begin;
+    int obs = blockIdx.y;
+    int64_t local = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x;
+    int64_t span = L.p_end - L.p_begin;
     if (local >= span) return;
+    if (L.unit_cpo > 0) {  // sharded launch (kernels.h unit mode)
+        if (!unit_coords(L, local, obs, local)) return;
+        span = L.n_particles;
+    }
     const int64_t particle = L.p_begin + local;
     const AdObsImg o = L.obs[obs];
     const uint64_t seed = L.seed;
@@ -53,7 +58,7 @@ __global__ void __launch_bounds__(kBlock) ad_particles_strict(const AdLaunch L) 
         x1 = x1 - floor(x1);
         x2 = x2 - floor(x2);
     }
-    L.values[static_cast<int64_t>(obs) * span + local] = scalar_eval(L.theta0, x1, x2);
+    ad_out_row(L, 0, obs, span)[local] = scalar_eval(L.theta0, x1, x2);
 }
 
 }  // namespace
@@ -61,7 +66,8 @@ __global__ void __launch_bounds__(kBlock) ad_particles_strict(const AdLaunch L) 
 cudaError_t launch_ad_particles_strict(const AdLaunch& L, cudaStream_t s) {
     const int64_t span = L.p_end - L.p_begin;
     if (span <= 0) return cudaSuccess;
-    const dim3 grid(static_cast<unsigned>((span + kBlock - 1) / kBlock), static_cast<unsigned>(L.n_obs), 1);
+    const dim3 grid(static_cast<unsigned>((span + kBlock - 1) / kBlock),
+                    static_cast<unsigned>(L.unit_cpo > 0 ? 1 : L.n_obs), 1);
     const int K = L.vel.is_constant ? 0 : L.vel.K;
     if (K <= 8) ad_particles_strict<8><<<grid, kBlock, 0, s>>>(L);
     else if (K <= 32) ad_particles_strict<32><<<grid, kBlock, 0, s>>>(L);

@@ -108,18 +108,19 @@ void check_particle_range(int64_t n_particles) {
     if (n_particles > (int64_t(1) << 32)) raise(SMC_ERUNTIME, "map_reduce: a particle work function threw");
 }
 
-AdPrepared prepare_ad(smc_ctx* ctx, const smc_ad_problem& p, const std::vector<const PreparedVelocity*>& fills,
-                      const PreparedVelocity& structure, int64_t obs_begin, int64_t obs_count) {
+AdImage build_ad_image(const smc_ad_problem& p, const std::vector<const PreparedVelocity*>& fills,
+                       const PreparedVelocity& structure, int64_t obs_begin, int64_t obs_count) {
     const double dt = ad_resolved_dt(p);
-    const double sigma = std::sqrt(2.0 * p.kappa);
-    Image im;
+    AdImage A;
+    A.sigma = std::sqrt(2.0 * p.kappa);
+    Image& im = A.im;
     std::vector<AdObsImg> obs;
-    AdPrepared out;
     for (int64_t j = obs_begin; j < obs_begin + obs_count; ++j) {
-        obs.push_back(make_ad_obs(p.obs_t[j], p.obs_x[2 * j], p.obs_x[2 * j + 1], dt, sigma));
-        out.steps_per_particle_sum += obs.back().n_steps;
+        obs.push_back(make_ad_obs(p.obs_t[j], p.obs_x[2 * j], p.obs_x[2 * j + 1], dt, A.sigma));
+        A.steps_per_particle_sum += obs.back().n_steps;
+        A.obs_steps.push_back(obs.back().n_steps);
     }
-    const size_t obs_off = im.add_vec(obs);
+    A.obs_off = im.add_vec(obs);
     // batched launches schedule the longest observations first (grid z), so
     // the short ones fill the tail instead of a long one trailing alone
     std::vector<int32_t> order(obs.size());
@@ -127,45 +128,61 @@ AdPrepared prepare_ad(smc_ctx* ctx, const smc_ad_problem& p, const std::vector<c
     if (std::getenv("SMC_NO_LPT") == nullptr)
         std::stable_sort(order.begin(), order.end(),
                          [&](int32_t a, int32_t b) { return obs[a].n_steps > obs[b].n_steps; });
-    const size_t order_off = im.add_vec(order);
-    const ScalarRef th = add_scalar(im, p.initial_condition);
-    const VelRef vr = add_velocity(im, structure, fills);
+    A.order_off = im.add_vec(order);
+    A.th = add_scalar(im, p.initial_condition);
+    A.vr = add_velocity(im, structure, fills);
     // Dense fields with K <= kDiskMaxK take the compile-time disk kernel.
-    size_t disk_off = 0;
     const bool disk = !structure.is_constant && p.precision != SMC_FP64_STRICT && structure.K <= kDiskMaxK &&
                       2 * structure.modes.size() >= static_cast<size_t>(disk_n_modes(structure.K)) &&
                       std::getenv("SMC_DISABLE_DISK") == nullptr;
     if (disk) {
         const size_t nc = static_cast<size_t>(disk_n_coef(structure.K));
-        disk_off = im.reserve(nc * fills.size() * sizeof(double));
+        A.disk_off = im.reserve(nc * fills.size() * sizeof(double));
         for (size_t b = 0; b < fills.size(); ++b)
-            disk_fill(structure.K, *fills[b], reinterpret_cast<double*>(im.bytes.data() + disk_off) + b * nc);
+            disk_fill(structure.K, *fills[b], reinterpret_cast<double*>(im.bytes.data() + A.disk_off) + b * nc);
         if (fills.size() == 1) {
-            const double* h = reinterpret_cast<const double*>(im.bytes.data() + disk_off);
-            out.host_disk.assign(h, h + nc);
+            const double* h = reinterpret_cast<const double*>(im.bytes.data() + A.disk_off);
+            A.host_disk.assign(h, h + nc);
         }
+        A.disk_K = structure.K;
     }
-    unsigned char* base = ctx->upload(im);
-    if (disk) {
-        out.disk_K = structure.K;
-        out.disk = reinterpret_cast<const double*>(base + disk_off);
+    A.obs_begin = obs_begin;
+    A.obs_count = obs_count;
+    A.n_particles = p.n_particles;
+    A.precision = p.precision;
+    return A;
+}
+
+AdPrepared upload_ad_image(smc_ctx* ctx, const AdImage& A) {
+    AdPrepared out;
+    unsigned char* base = ctx->upload(A.im);
+    out.host_disk = A.host_disk;
+    if (A.disk_K > 0) {
+        out.disk_K = A.disk_K;
+        out.disk = reinterpret_cast<const double*>(base + A.disk_off);
     }
+    out.steps_per_particle_sum = A.steps_per_particle_sum;
     AdLaunch& L = out.L;
-    L.vel = patch(vr, base);
-    L.theta0 = patch(th, base);
-    L.obs = reinterpret_cast<const AdObsImg*>(base + obs_off);
-    L.obs_order = reinterpret_cast<const int32_t*>(base + order_off);
-    L.n_obs = static_cast<int32_t>(obs_count);
-    L.obs_slot0 = static_cast<uint32_t>(obs_begin);
-    L.n_particles = p.n_particles;
+    L.vel = patch(A.vr, base);
+    L.theta0 = patch(A.th, base);
+    L.obs = reinterpret_cast<const AdObsImg*>(base + A.obs_off);
+    L.obs_order = reinterpret_cast<const int32_t*>(base + A.order_off);
+    L.n_obs = static_cast<int32_t>(A.obs_count);
+    L.obs_slot0 = static_cast<uint32_t>(A.obs_begin);
+    L.n_particles = A.n_particles;
     L.p_begin = 0;
-    L.p_end = p.n_particles;
+    L.p_end = A.n_particles;
     L.n_samples = 1;
-    L.precision = p.precision;
-    L.sigma = sigma;
+    L.precision = A.precision;
+    L.sigma = A.sigma;
     L.host_disk = out.host_disk.empty() ? nullptr : out.host_disk.data();
-    out.n_obs = obs_count;
+    out.n_obs = A.obs_count;
     return out;
+}
+
+AdPrepared prepare_ad(smc_ctx* ctx, const smc_ad_problem& p, const std::vector<const PreparedVelocity*>& fills,
+                      const PreparedVelocity& structure, int64_t obs_begin, int64_t obs_count) {
+    return upload_ad_image(ctx, build_ad_image(p, fills, structure, obs_begin, obs_count));
 }
 
 void run_particles(smc_ctx* ctx, AdLaunch& L, const AdPrepared* P, int64_t sample0) {
@@ -386,6 +403,7 @@ smc_status smc_create(int device, smc_ctx** out) {
 
 void smc_destroy(smc_ctx* ctx) {
     if (!ctx) return;
+    if (ctx->group) group_destroy(ctx);  // the other members and the communicators
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->own_stream) cudaStreamSynchronize(ctx->own_stream);
@@ -454,7 +472,8 @@ int64_t smc_num_chunks(int64_t n_particles) { return (n_particles + kChunk - 1) 
 smc_status smc_ad_observe(smc_ctx* ctx, const smc_ad_problem* p, uint64_t seed, smc_estimate* out) {
     return guarded(__func__, [&] {
         CK(cudaSetDevice(ctx->device));
-        ad_observe_range(ctx, *p, seed, 0, p->n_obs, out);
+        if (is_sharded(ctx)) group_ad_observe(ctx, *p, seed, 0, p->n_obs, out);
+        else ad_observe_range(ctx, *p, seed, 0, p->n_obs, out);
     });
 }
 
@@ -469,73 +488,8 @@ smc_status smc_ad_observe_single(smc_ctx* ctx, const smc_ad_problem* p, uint64_t
         ad_validate(*p);
         if (obs_index >= static_cast<uint64_t>(p->n_obs))
             raise(SMC_ERANGE, "observe_ad_single: observation index out of range");
-        ad_observe_range(ctx, *p, seed, static_cast<int64_t>(obs_index), 1, out);
-    });
-}
-
-smc_status smc_ad_shard_partials(smc_ctx* ctx, const smc_ad_problem* p, uint64_t seed, int64_t chunk_begin,
-                                 int64_t chunk_end, double* partials_dev) {
-    return guarded(__func__, [&] {
-        CK(cudaSetDevice(ctx->device));
-        const PreparedVelocity v = prepare_velocity(p->velocity);
-        check_kappa(p->kappa);
-        check_scalar(p->initial_condition);
-        ad_validate(*p);
-        check_particle_range(p->n_particles);
-        const int64_t n_chunks = smc_num_chunks(p->n_particles);
-        if (chunk_begin < 0 || chunk_end > n_chunks || chunk_begin > chunk_end)
-            raise(SMC_ERANGE, "smc_ad_shard_partials: chunk range out of bounds");
-        if (p->n_obs > 65535) raise(SMC_ERUNTIME, "smc_ad_shard_partials: at most 65535 observations per shard launch");
-        ctx->stats = smc_stats{};
-        AdPrepared P = prepare_ad(ctx, *p, {&v}, v, 0, p->n_obs);
-        P.L.seed = seed;
-        P.L.p_begin = chunk_begin * kChunk;
-        P.L.p_end = std::min(chunk_end * kChunk, p->n_particles);
-        const int64_t span = std::max<int64_t>(P.L.p_end - P.L.p_begin, 0);
-        P.L.values = ctx->values.get<double>(static_cast<size_t>(std::max<int64_t>(p->n_obs * span, 1)));
-        CK(cudaEventRecord(ctx->ev[0], ctx->stream));
-        run_particles(ctx, P.L, &P);
-        CK(cudaEventRecord(ctx->ev[1], ctx->stream));
-        const int64_t nloc = chunk_end - chunk_begin;
-        if (nloc > 0) {
-            CK(launch_tree_pass(P.L.values, span, nullptr, span, p->n_obs, partials_dev, nloc, nullptr, 0, ctx->stream));
-            count_launches(ctx, 1);
-        }
-        CK(cudaEventRecord(ctx->ev[2], ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
-        finish_stats(ctx);
-        ctx->shard_n_obs = p->n_obs;
-        ctx->shard_span = span;
-        ctx->stats.particle_steps = P.steps_per_particle_sum * span;
-    });
-}
-
-smc_status smc_tree_finish(smc_ctx* ctx, const double* partials_dev, int64_t n_obs, int64_t n_chunks,
-                           double* sums_dev) {
-    return guarded(__func__, [&] {
-        CK(cudaSetDevice(ctx->device));
-        double* scratch = ctx->scratch.get<double>(static_cast<size_t>(2 * n_obs * std::max<int64_t>(1, n_chunks)));
-        int launches = 0;
-        CK(tree_reduce(partials_dev, n_chunks, nullptr, n_chunks, n_obs, sums_dev, nullptr, 0, scratch, ctx->stream,
-                       &launches));
-        count_launches(ctx, launches);
-        CK(cudaStreamSynchronize(ctx->stream));
-    });
-}
-
-smc_status smc_ad_shard_sq_partials(smc_ctx* ctx, const double* means_dev, int64_t n_obs, int64_t chunk_begin,
-                                    int64_t chunk_end, double* partials_dev) {
-    return guarded(__func__, [&] {
-        CK(cudaSetDevice(ctx->device));
-        if (n_obs != ctx->shard_n_obs) raise(SMC_EINVAL, "smc_ad_shard_sq_partials: observation count mismatch");
-        const int64_t nloc = chunk_end - chunk_begin;
-        const int64_t span = ctx->shard_span;
-        if (nloc > 0) {
-            CK(launch_tree_pass(static_cast<const double*>(ctx->values.p), span, nullptr, span, n_obs, partials_dev,
-                                nloc, means_dev, 1, ctx->stream));
-            count_launches(ctx, 1);
-        }
-        CK(cudaStreamSynchronize(ctx->stream));
+        if (is_sharded(ctx)) group_ad_observe(ctx, *p, seed, static_cast<int64_t>(obs_index), 1, out);
+        else ad_observe_range(ctx, *p, seed, static_cast<int64_t>(obs_index), 1, out);
     });
 }
 
@@ -677,53 +631,16 @@ smc_status smc_bvp_observe_range(smc_ctx* ctx, const smc_bvp_problem* p, uint64_
         if (obs_begin < 0 || obs_count < 0 || obs_begin + obs_count > p->n_obs)
             raise(SMC_ERANGE, "observe_bvp: observation range out of bounds");
         CK(cudaSetDevice(ctx->device));
+        if (is_sharded(ctx)) {
+            group_bvp_observe(ctx, *p, seed, obs_begin, obs_count, out);
+            return;
+        }
         ctx->stats = smc_stats{};
         BvpLaunch L = prepare_bvp(ctx, *p, obs_begin, obs_count);
         L.seed = seed;
         const int64_t n = p->n_particles, n_obs = obs_count;
         run_bvp(ctx, L, n_obs, n);
         reduce_bvp(ctx, L.values, L.aux, L.failed, n, n_obs, L.step_total, out);
-    });
-}
-
-smc_status smc_bvp_shard_values(smc_ctx* ctx, const smc_bvp_problem* p, uint64_t seed, int64_t walker_begin,
-                                int64_t walker_end, double* values_dev, double* aux_dev, uint8_t* failed_dev) {
-    return guarded(__func__, [&] {
-        if (walker_begin < 0 || walker_end > p->n_particles || walker_begin > walker_end)
-            raise(SMC_ERANGE, "smc_bvp_shard_values: walker range out of bounds");
-        CK(cudaSetDevice(ctx->device));
-        ctx->stats = smc_stats{};
-        BvpLaunch L = prepare_bvp(ctx, *p, 0, p->n_obs);
-        L.seed = seed;
-        const int64_t span = walker_end - walker_begin;
-        if (span == 0) return;
-        L.n_particles = span;
-        L.p_begin = walker_begin;
-        run_bvp(ctx, L, p->n_obs, span);
-        cudaStream_t s = ctx->stream;
-        const size_t total = static_cast<size_t>(p->n_obs * span);
-        CK(cudaMemcpyAsync(values_dev, L.values, total * sizeof(double), cudaMemcpyDeviceToDevice, s));
-        CK(cudaMemcpyAsync(aux_dev, L.aux, total * sizeof(double), cudaMemcpyDeviceToDevice, s));
-        CK(cudaMemcpyAsync(failed_dev, L.failed, total, cudaMemcpyDeviceToDevice, s));
-        unsigned long long* steps_h = ctx->staging.get<unsigned long long>(1);
-        CK(cudaMemcpyAsync(steps_h, L.step_total, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-        CK(cudaEventRecord(ctx->ev[2], s));
-        CK(cudaStreamSynchronize(s));
-        ctx->stats.particle_steps = static_cast<int64_t>(*steps_h);
-        finish_stats(ctx);
-    });
-}
-
-smc_status smc_bvp_reduce_values(smc_ctx* ctx, const double* values_dev, const double* aux_dev,
-                                 const uint8_t* failed_dev, int64_t n_walkers, int64_t n_obs, smc_estimate* out) {
-    return guarded(__func__, [&] {
-        if (n_walkers < 2 || n_obs < 1)
-            raise(SMC_EINVAL, "smc_bvp_reduce_values: need >= 2 walkers and >= 1 observation");
-        CK(cudaSetDevice(ctx->device));
-        ctx->stats = smc_stats{};
-        CK(cudaEventRecord(ctx->ev[0], ctx->stream));
-        CK(cudaEventRecord(ctx->ev[1], ctx->stream));
-        reduce_bvp(ctx, values_dev, aux_dev, failed_dev, n_walkers, n_obs, nullptr, out);
     });
 }
 

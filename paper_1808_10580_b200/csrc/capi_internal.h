@@ -144,20 +144,36 @@ using smc::capi::DevBuf;
 using smc::capi::Image;
 using smc::capi::PinnedBuf;
 
+// Multi-device group (capi_group.cu): the ranks of one
+// sharded forward map.  Single process: members are per-device contexts of
+// this process (members[0] is the owning context).  One process per GPU:
+// one member, rank0 = this process's rank.  comms: one ncclComm_t per member
+// (empty: the emulated exchange of a single process with repeated devices).
+struct smc_group {
+    int world = 1;
+    int rank0 = 0;
+    std::vector<smc_ctx*> members;
+    std::vector<void*> comms;
+    std::vector<cudaEvent_t> ready;  // per member: contribution enqueued (emulated exchange)
+    smc_exchange_fn hook = nullptr;  // host-staged exchange (smc_create_rank_hosted)
+    void* hook_user = nullptr;
+    PinnedBuf hook_buf;
+};
+
 struct smc_ctx {
     int device = 0;
+    smc_group* group = nullptr;         // non-null: multi-device context (see smc_group)
     cudaStream_t stream = nullptr;      // stream every launch goes to
     cudaStream_t own_stream = nullptr;  // the context's own stream
     int64_t total_launches = 0;
     cudaEvent_t ev[4] = {};
     DevBuf image, values, aux, flags, flags2, scratch, sums, means, sumsq, sumaux, est, counts, tmp_a, tmp_b, tmp_c;
     DevBuf chunk_tmp;  // compaction scan scratch of smc_bvp_forcing_basis
+    DevBuf gx_a, gx_b, gx_c, gx_d;  // group exchange buffers (every rank's contribution)
     DevBuf pk_ip, pk_im, pk_kp, pk_km, pk_ms, pk_u, pk_blocks, pk_bad;  // device u -> field packing
     DevBuf gal_A, gal_t0, gal_t1, gal_k1, gal_k2, gal_obs, gal_grid;  // Galerkin reference solver
     PinnedBuf staging, est_host;
     smc_stats stats{};
-    // sharded AD state (smc_ad_shard_*)
-    int64_t shard_n_obs = 0, shard_span = 0;
 
     unsigned char* upload(const Image& img) {
         unsigned char* h = staging.get<unsigned char>(img.bytes.size());
@@ -199,6 +215,25 @@ struct AdPrepared {
     int64_t n_obs = 0;
     int64_t steps_per_particle_sum = 0;  // sum_j n_j
 };
+// The device-independent part of an AD launch: the host image and the offsets
+// to patch after upload (multi-device groups build it once and upload it to
+// every member).
+struct AdImage {
+    Image im;
+    size_t obs_off = 0, order_off = 0, disk_off = 0;
+    ScalarRef th;
+    VelRef vr;
+    int disk_K = 0;
+    std::vector<double> host_disk;
+    std::vector<int64_t> obs_steps;  // n_j per image observation
+    int64_t steps_per_particle_sum = 0;
+    int64_t obs_begin = 0, obs_count = 0, n_particles = 0;
+    int32_t precision = 0;
+    double sigma = 0.0;
+};
+AdImage build_ad_image(const smc_ad_problem& p, const std::vector<const PreparedVelocity*>& fills,
+                       const PreparedVelocity& structure, int64_t obs_begin, int64_t obs_count);
+AdPrepared upload_ad_image(smc_ctx* ctx, const AdImage& A);
 void check_particle_range(int64_t n_particles);
 AdPrepared prepare_ad(smc_ctx* ctx, const smc_ad_problem& p, const std::vector<const PreparedVelocity*>& fills,
                       const PreparedVelocity& structure, int64_t obs_begin, int64_t obs_count);
@@ -212,6 +247,14 @@ void ad_observe_range(smc_ctx* ctx, const smc_ad_problem& p, uint64_t seed, int6
                       smc_estimate* out);
 BvpLaunch prepare_bvp(smc_ctx* ctx, const smc_bvp_problem& p, int64_t obs_begin, int64_t obs_count);
 void run_bvp(smc_ctx* ctx, BvpLaunch& L, int64_t n_obs, int64_t n);
+// Multi-device groups (capi_group.cu).  is_sharded: the context is a group of
+// more than one rank, so the forward maps run sharded.
+inline bool is_sharded(const smc_ctx* ctx) { return ctx->group != nullptr; }
+void group_destroy(smc_ctx* ctx);
+void group_ad_observe(smc_ctx* ctx, const smc_ad_problem& p, uint64_t seed, int64_t obs_begin, int64_t obs_count,
+                      smc_estimate* out);
+void group_bvp_observe(smc_ctx* ctx, const smc_bvp_problem& p, uint64_t seed, int64_t obs_begin, int64_t obs_count,
+                       smc_estimate* out);
 // Upload a PackMap into the context's pack buffers (reused across calls).
 PackDev upload_pack_map(smc_ctx* ctx, const PackMap& m);
 

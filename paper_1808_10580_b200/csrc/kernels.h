@@ -35,9 +35,20 @@ struct AdLaunch {
     const double* host_disk;   // host copy of the single-sample disk coefficient block (or null)
     const int32_t* obs_order;  // [n_obs] observations by decreasing step count
     int32_t obs_major;         // batched grid order: 1 = (blocks, samples, obs longest first), 0 = (blocks, obs, samples)
-    int32_t pad_;
+    int32_t unit_cpo;          // > 0: unit mode (sharded single-sample launch), = chunks per observation
+    int64_t unit0;             // unit mode: first (observation, chunk) unit, unit = obs * unit_cpo + chunk
     RoundKeys rk;              // Philox round keys of `seed` (filled by the launcher that uses them)
 };
+
+// Unit mode (multi-GPU sharding of one evaluation): a launch
+// covers the (observation, chunk) units [unit0, unit0 + n_units) of the
+// image's observations, with p_begin = 0 and p_end = n_units * kChunk.  The
+// flat thread index f maps to unit unit0 + f / kChunk and particle
+// (unit % unit_cpo) * kChunk + f % kChunk of observation unit / unit_cpo, and
+// its terminal value lands at values[f] (chunk-contiguous), so a chunk tree
+// over values[u * kChunk ...] is that unit's exact aligned partial.  Threads
+// past their observation's last particle do nothing (the partial kernel masks
+// them).  Grid y = 1.
 
 cudaError_t launch_ad_particles(const AdLaunch& L, cudaStream_t s);
 // Batched grid order (AdLaunch::obs_major) for a launch of this shape.
@@ -107,6 +118,23 @@ cudaError_t compact_valid(const double* values, const double* aux, const uint8_t
 cudaError_t launch_tree_pass(const double* in, int64_t in_stride, const int64_t* counts,
                              int64_t n_uniform, int64_t n_seg, double* out, int64_t out_stride,
                              const double* center, int mode, cudaStream_t s);
+
+// Sharded AD: the chunk partial of each unit [unit0, unit0 + n_units) from the
+// unit-mode K1 values (chunk-contiguous); out[u - unit0].  mode 0: x_i;
+// mode 1: (x_i - center[obs])^2.
+cudaError_t launch_unit_partials(const double* values, int64_t n_units, int64_t unit0, int64_t cpo,
+                                 int64_t n_particles, const double* center, int mode, double* out, cudaStream_t s);
+
+// Sharded Dirichlet reduction (reduce_kernels.cu): this rank's compacted valid
+// walkers of every observation -> the tree sums of the aligned dyadic blocks of
+// its interval in the global compacted order, kDyadicSlots per (obs, quantity);
+// and the receiver's merge of all ranks' blocks into the per-observation sums.
+constexpr int kDyadicSlots = 64;
+cudaError_t launch_dyadic_blocks(const double* vals, int64_t qstride, int nq, int64_t vstride, const int64_t* gcounts,
+                                 int world, int rank, int64_t n_obs, const double* center, int mode, double* rec,
+                                 double* scratch, int64_t sstride, cudaStream_t s);
+cudaError_t launch_dyadic_finish(const double* rec, const int64_t* gcounts, int world, int64_t n_obs, int nq,
+                                 double* sums, int64_t* counts_total, double* means, cudaStream_t s);
 
 // Runs tree passes until one value per segment remains.  scratch must hold
 // 2 * n_seg * ceil(n/1024) doubles.  counts may be null (all segments n).

@@ -63,7 +63,7 @@ def test_c2_full_particle_prefix_matches_oracle(ctx, port, c2):
 def test_c2_full_sharded_bit_identical(ctx, c2):
     spec, est = c2
     for world in (2, 8):
-        assert D.observe_ad_emulated(spec, 808, world, ctx) == est
+        assert S.observe_ad(spec, 808, ctx=S.Context(devices=[0] * world)) == est
 
 
 def test_c3_full_observation_split_and_prefix(ctx, port):

@@ -282,13 +282,12 @@ def test_validation_errors_on_device_path(ctx):
 # ------------------------------------------------ sharded (multi-GPU) path ----
 @pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
 def test_sharded_partials_are_bit_identical(ctx, world):
-    from paper_1808_10580_b200 import distributed as D
     u = S.prior_draw(specs.C2_PRIOR, 808, 0xBE9C4, 0, ctx)
     spec = specs.c2_spec(u, n_particles=5000)
     spec.observations = spec.observations[:3]
     spec.observations = [S.AdObservation(0.2, o.x) for o in spec.observations]
     whole = S.observe_ad(spec, 808, ctx=ctx)
-    est = D.observe_ad_emulated(spec, 808, world, ctx)
+    est = S.observe_ad(spec, 808, ctx=S.Context(devices=[0] * world))
     for a, b in zip(whole, est):
         assert a.mean == b.mean and a.std_error == b.std_error
 
@@ -312,16 +311,15 @@ def test_more_observations_than_one_grid_dimension(ctx):
 @pytest.mark.parametrize("max_steps", [10_000_000, 150])
 @pytest.mark.parametrize("world", [2, 3, 8])
 def test_bvp_walker_sharding_bit_identical(ctx, world, max_steps):
-    """SURVEY.md 8(e) for the Dirichlet map: walker ranges per rank, per-walker
-    results all-gathered in walker order, one reduction — equal to observe_bvp
-    bit for bit for any split, including runs where walkers fail (max_steps
-    150: the compaction before the reference's tree then depends on failures
-    in other ranks' ranges)."""
-    from paper_1808_10580_b200 import distributed as D
+    """SURVEY.md 8(e) for the Dirichlet map: walker ranges per rank, valid
+    counts and aligned dyadic block sums exchanged — equal to observe_bvp bit
+    for bit for any split, including runs where walkers fail (max_steps 150:
+    the compaction before the reference's tree then depends on failures in
+    other ranks' ranges)."""
     spec = specs.paper_bvp(n_particles=5000)
     spec.max_steps = max_steps
     want = S.observe_bvp(spec, 606, ctx=ctx)
-    got = D.observe_bvp_emulated(spec, 606, world, ctx=ctx)
+    got = S.observe_bvp(spec, 606, ctx=S.Context(devices=[0] * world))
     if max_steps == 150:
         assert sum(e.n_failed for e in want) > 0
     for a, b in zip(got, want):
