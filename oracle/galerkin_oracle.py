@@ -85,7 +85,7 @@ def project(theta0, modes) -> np.ndarray:
             theta[i] += c
 
     kind = theta0.kind
-    from paper_1808_10580_b200 import _abi as A
+    from oracle import pods as A
     if kind == A.SCALAR_CONSTANT:
         place(0, 0, theta0.constant_value)
         return theta

@@ -18,7 +18,7 @@ from pathlib import Path
 
 import numpy as np
 
-from paper_1808_10580_b200 import _abi as A
+from oracle import pods as A  # the checkers' own copy of the ABI PODs (no product import)
 
 HERE = Path(__file__).resolve().parent
 PORT_LIB = HERE / "liboracle.so"

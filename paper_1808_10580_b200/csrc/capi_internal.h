@@ -251,6 +251,11 @@ void run_bvp(smc_ctx* ctx, BvpLaunch& L, int64_t n_obs, int64_t n);
 // more than one rank, so the forward maps run sharded.
 inline bool is_sharded(const smc_ctx* ctx) { return ctx->group != nullptr; }
 void group_destroy(smc_ctx* ctx);
+// All-gather of variable-size byte slices: rank r's slice [displ[r], +bytes[r])
+// of bufs[m] (member m's device buffer) is in place on its owner; afterwards
+// every member holds every slice.  Enqueued on the members' streams.
+void group_exchange(smc_group* g, const std::vector<unsigned char*>& bufs, const std::vector<size_t>& displ,
+                    const std::vector<size_t>& bytes);
 void group_ad_observe(smc_ctx* ctx, const smc_ad_problem& p, uint64_t seed, int64_t obs_begin, int64_t obs_count,
                       smc_estimate* out);
 void group_bvp_observe(smc_ctx* ctx, const smc_bvp_problem& p, uint64_t seed, int64_t obs_begin, int64_t obs_count,

@@ -169,3 +169,45 @@ def test_repeated_group_calls_reuse_buffers(ctx):
         assert same(S.observe_ad(spec, 808, ctx=g), S.observe_ad(spec, 808, ctx=ctx))
         bvp = specs.paper_bvp(n_particles=n)
         assert same(S.observe_bvp(bvp, 606, ctx=g), S.observe_bvp(bvp, 606, ctx=ctx))
+
+
+# ---------------------------------------------------- batched and pCN ------
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_batched_group_sample_sharding(ctx, world):
+    prior = specs.C2_PRIOR
+    u0 = S.prior_draw(prior, 808, 0xBE9C4, 0, ctx)
+    U = np.stack([u0 * (1.0 + 0.01 * b) for b in range(7)])
+    base = specs.c4_base(n_particles=500)
+    want = S.observe_ad_batched(base, prior, U, 808, ctx=ctx)
+    got = S.observe_ad_batched(base, prior, U, 808, ctx=group(world))
+    assert got.tobytes() == want.tobytes()
+    seeds = np.arange(7, dtype=np.uint64) + 100
+    want = S.observe_ad_batched(base, prior, U, 808, seeds=seeds, ctx=ctx)
+    got = S.observe_ad_batched(base, prior, U, 808, seeds=seeds, ctx=group(world))
+    assert got.tobytes() == want.tobytes()
+
+
+def test_batched_group_non_finite_raises(ctx):
+    prior = specs.C2_PRIOR
+    U = np.zeros((4, prior.dimension()))
+    U[3, 5] = np.nan
+    base = specs.c4_base(n_particles=64)
+    with pytest.raises(ValueError, match="non-finite"):
+        S.observe_ad_batched(base, prior, U, 808, ctx=group(2))
+
+
+PCN_DATA = [-0.9065, -0.7528, -0.6665, -0.8091, -0.6508, -0.5135, -0.5185, -0.4553, -0.4066]
+
+
+@pytest.mark.parametrize("world,chains", [(2, 5), (3, 2), (8, 9)])
+def test_pcn_group_chain_sharding(ctx, world, chains):
+    fwd = specs.c4_base(n_particles=160)
+    fwd.dt = 0.006
+    like = S.LikelihoodSpec(data=PCN_DATA, noise_std=0.05, forward=fwd, forward_seed=1234)
+    prior = S.PriorSpec(2, 0.6, 2.5)
+    cfg = S.ChainConfig(n_steps=12, beta=0.3, burn_in=2, thin=3)
+    seeds = list(range(40, 40 + chains))
+    want = S.run_chains(cfg, prior, like, seeds, ctx=ctx)
+    got = S.run_chains(cfg, prior, like, seeds, ctx=group(world))
+    for k in ("final_u", "final_phi", "map_u", "map_objective", "accepted", "phi_trace", "samples"):
+        assert np.array_equal(got[k], want[k]), k

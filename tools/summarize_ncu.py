@@ -59,6 +59,13 @@ WANT = {
     "smsp__inst_executed.sum": "warp_instructions",
     "sm__cycles_elapsed.avg": "sm_cycles_elapsed",
     "smsp__cycles_active.avg": "smsp_cycles_active",
+    "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum": "thread_dfma",
+    "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum": "thread_dadd",
+    "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum": "thread_dmul",
+    "smsp__sass_thread_inst_executed_op_ffma_pred_on.sum": "thread_ffma",
+    "smsp__sass_thread_inst_executed_op_fadd_pred_on.sum": "thread_fadd",
+    "smsp__sass_thread_inst_executed_op_fmul_pred_on.sum": "thread_fmul",
+    "smsp__thread_inst_executed.sum": "thread_instructions",
 }
 
 
@@ -99,6 +106,16 @@ def full(rep: Path, out: Path, units: float | None) -> None:
     if units:
         res["units_per_launch"] = units
         res["dram_bytes_per_unit"] = res["dram_bytes_per_launch"] / units
+        # the FP64 (FP32) flops the kernel actually executes per unit: 2 per
+        # FMA, 1 per add / mul thread-instruction (predicated-on)
+        if res.get("thread_dfma") is not None:
+            res["executed_fp64_flops_per_unit"] = (2 * res["thread_dfma"] + (res.get("thread_dadd") or 0) +
+                                                   (res.get("thread_dmul") or 0)) / units
+        if res.get("thread_ffma") is not None:
+            res["executed_fp32_flops_per_unit"] = (2 * res["thread_ffma"] + (res.get("thread_fadd") or 0) +
+                                                   (res.get("thread_fmul") or 0)) / units
+        if res.get("thread_instructions") is not None:
+            res["thread_instructions_per_unit"] = res["thread_instructions"] / units
     out.with_suffix(".json").write_text(json.dumps(res, indent=1) + "\n")
     md = [f"# ncu --set full: {res['kernel'][:120]}", "", f"report `{rep.name}`", "", "| metric | value |", "|---|---|"]
     for k, v in res.items():
