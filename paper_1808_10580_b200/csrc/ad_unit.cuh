@@ -7,9 +7,15 @@
 namespace smc {
 
 // Unit mode (kernels.h): the observation and particle of flat thread index
-// `flat`; false for a thread past its observation's last particle.
+// `flat`; false for a thread past its observation's last particle.  The unit
+// (hence the observation, its step count and the loop counter) is derived from
+// the block's first index only: block sizes divide kChunk, so it is the same
+// for every thread, and keeping it block-uniform keeps the step loop's counter
+// in a uniform register (the disk kernel's coefficient loads depend on that,
+// ad_disk.cu).
 __device__ __forceinline__ bool unit_coords(const AdLaunch& L, int64_t flat, int& obs, int64_t& local) {
-    const int64_t unit = L.unit0 + flat / kChunk;
+    const int64_t block_first = static_cast<int64_t>(blockIdx.x) * blockDim.x;
+    const int64_t unit = L.unit0 + block_first / kChunk;
     const int64_t o = unit / L.unit_cpo;
     obs = static_cast<int>(o);
     local = (unit - o * L.unit_cpo) * kChunk + (flat % kChunk);
