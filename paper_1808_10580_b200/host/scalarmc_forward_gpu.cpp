@@ -18,8 +18,11 @@
 //
 // Build: compile against the reference's include directory and
 // link libscalarmc_b200.so instead of forward_ad.o and forward_bvp.o.
-// `workers` is ignored: the device is chosen by SCALARMC_DEVICE (default
-// LOCAL_RANK, else 0).  SCALARMC_PRECISION=fp32|fp64_strict selects the
+// `workers` (the reference's thread count, executor.cpp:45-85) is ignored:
+// the parallelism is the GPU set.  SCALARMC_DEVICES=0,1,...,7 makes the forward
+// maps shard over those GPUs of the box (smc_create_multi: NCCL exchange,
+// results bit-identical to one GPU, so run_chain and every other caller scale
+// unchanged); otherwise one device, SCALARMC_DEVICE (default LOCAL_RANK, else 0).  SCALARMC_PRECISION=fp32|fp64_strict selects the
 // optional FP32 mode or the strict diagnostic build.
 #include <cstdlib>
 #include <cstring>
@@ -58,6 +61,20 @@ struct Device {
 Device& device() {
     static Device d;
     std::call_once(d.once, [&] {
+        if (const char* list = std::getenv("SCALARMC_DEVICES")) {
+            std::vector<int> devs;
+            for (const char* p = list; *p;) {
+                char* end = nullptr;
+                const long v = std::strtol(p, &end, 10);
+                if (end == p) break;
+                devs.push_back(static_cast<int>(v));
+                p = (*end == ',') ? end + 1 : end;
+            }
+            if (!devs.empty()) {
+                d.init_status = smc_create_multi(static_cast<int>(devs.size()), devs.data(), &d.ctx);
+                return;
+            }
+        }
         int dev = 0;
         if (const char* e = std::getenv("SCALARMC_DEVICE")) dev = std::atoi(e);
         else if (const char* r = std::getenv("LOCAL_RANK")) dev = std::atoi(r);

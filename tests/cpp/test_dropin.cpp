@@ -133,6 +133,9 @@ int main() {
         cc.seed = 31337;
         const auto res = run_chain(cc, prior, &like);
         emit_ok("pcn_chain_runs", res.phi_trace.size() == 20 && std::isfinite(res.map_objective));
+        emit_value("pcn_map_objective", res.map_objective);
+        emit_value("pcn_acceptance_rate", res.acceptance_rate);
+        emit_value("pcn_last_phi", res.phi_trace.back());
     }
 
     // 5. observe_bvp and forcing_cost (optimize.cpp:161-173) over the GPU map.

@@ -8,6 +8,7 @@ run_chain and forcing_cost call the GPU forward map exactly as they would in a
 scalarmc build.  The numbers must match the golden fixtures of the real
 reference within the FP64 parity gate."""
 import json
+import os
 import subprocess
 from pathlib import Path
 
@@ -18,16 +19,34 @@ from conftest import est_from
 BIN = Path(__file__).resolve().parent / "cpp" / "_bin" / "test_dropin"
 
 
-@pytest.mark.gpu
-def test_cpp_dropin_under_reference_callers(golden):
+def run_dropin(env=None):
     if not BIN.exists():
         pytest.skip("tests/cpp/_bin/test_dropin not built (needs the reference headers at build time)")
-    out = subprocess.run([str(BIN)], capture_output=True, text=True, timeout=600)
+    out = subprocess.run([str(BIN)], capture_output=True, text=True, timeout=600,
+                         env=dict(os.environ, **(env or {})))
     assert out.returncode == 0, out.stderr
     checks = {}
     for line in out.stdout.splitlines():
         rec = json.loads(line)
         checks[rec["check"]] = rec
+    return checks
+
+
+@pytest.mark.gpu
+def test_cpp_dropin_multi_device_bit_identical():
+    """SCALARMC_DEVICES puts the unchanged reference callers (misfit,
+    run_chain, forcing_cost, the CLI bodies) on a multi-device context; with
+    the one B200 the list repeats device 0 (emulated exchange, same shard
+    plans).  Every number must equal the one-device run bit for bit."""
+    one = run_dropin()
+    for devs in ("0,0", "0,0,0,0,0,0,0,0"):
+        many = run_dropin({"SCALARMC_DEVICES": devs})
+        assert many == one, devs
+
+
+@pytest.mark.gpu
+def test_cpp_dropin_under_reference_callers(golden):
+    checks = run_dropin()
     bad = [k for k, v in checks.items() if v.get("ok") is False]
     assert not bad, {k: checks[k] for k in bad}
 
