@@ -14,7 +14,9 @@ from pathlib import Path
 import numpy as np
 
 PKG_DIR = Path(__file__).resolve().parent
-LIB_PATH = PKG_DIR / "lib" / "libscalarmc_b200.so"
+# SMC_LIBRARY: an alternative build of the same library (A/B measurements of
+# two kernel versions on one box); the default is the in-tree build.
+LIB_PATH = Path(os.environ.get("SMC_LIBRARY") or PKG_DIR / "lib" / "libscalarmc_b200.so")
 
 SMC_OK, SMC_EINVAL, SMC_ERANGE, SMC_ERUNTIME, SMC_ECUDA = range(5)
 SCALAR_CONSTANT, SCALAR_COSINE, SCALAR_BUMPS, SCALAR_LINEAR = range(4)

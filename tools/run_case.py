@@ -107,7 +107,7 @@ if args.config in ("c3", "c3b"):
           f"{st.particle_steps} -> {st.particle_steps / st.particle_kernel_ms * 1e3:.4g} walker-steps/s; "
           f"mean[0]={est[0].mean:.15g} exit[0]={est[0].aux_mean:.6g} failed={sum(e.n_failed for e in est)}")
     sys.exit(0)
-kind, spec, steps, F, desc = bench.build_workload(args.config, ctx)
+kind, spec, steps = bench.build_workload(args.config, ctx)
 if args.cutoff:
     import specs
     prior = S.PriorSpec(args.cutoff, 1.0, 2.5)
