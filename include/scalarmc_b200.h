@@ -390,6 +390,15 @@ smc_status smc_fp64_peak(smc_ctx* ctx, double ms, double* tflops);
  * SMC_FP32 variant. */
 smc_status smc_fp32_peak(smc_ctx* ctx, double ms, double* tflops);
 
+/* Guard-zone self-test (diagnostic; the GPU pool refuses compute-sanitizer).
+ * With SMC_GUARD=1 in the environment every device buffer carries 4 KB guard
+ * zones before and after it, checked at the end of every C-ABI call.  This
+ * entry writes `nbytes` zero bytes at byte `offset` of a 1024-byte context
+ * buffer: an offset range outside [0, 1024) must fail with SMC_ERUNTIME
+ * ("device buffer overrun ...").  Returns SMC_EINVAL when guard mode is off
+ * (the write would land outside any buffer). */
+smc_status smc_guard_selftest(smc_ctx* ctx, int64_t offset, int64_t nbytes);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -173,6 +173,7 @@ _PROTOS = {
                                           C.c_int64, _dp]),
     "smc_last_stats": (C.c_int, [C.c_void_p, C.POINTER(smc_stats)]),
     "smc_fp64_peak": (C.c_int, [C.c_void_p, C.c_double, _dp]),
+    "smc_guard_selftest": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64]),
     "smc_fp32_peak": (C.c_int, [C.c_void_p, C.c_double, _dp]),
     "smc_struct_sizes": (C.c_int, [C.POINTER(C.c_int64), C.c_int]),
 }

@@ -7,6 +7,9 @@
 // particle kernel -> K3 tree reduction passes -> estimates kernel -> one D2H
 // copy of n_obs x 40 B.  All on the context's stream; persistent buffers grow
 // and are reused across calls.
+#include <mutex>
+#include <set>
+
 #include "capi_internal.h"
 
 using namespace smc;
@@ -15,6 +18,95 @@ using namespace smc::capi;
 namespace smc::capi {
 
 thread_local std::string g_err;
+
+// ---- guard zones (SMC_GUARD=1) ----------------------------------------------
+namespace {
+std::mutex g_guard_mu;
+std::set<DevBuf*>& guard_registry() {
+    static std::set<DevBuf*> r;
+    return r;
+}
+}  // namespace
+
+bool guard_mode() {
+    static const bool on = [] {
+        const char* e = std::getenv("SMC_GUARD");
+        return e && *e && std::strcmp(e, "0") != 0;
+    }();
+    return on;
+}
+
+void DevBuf::allocate_guarded(size_t bytes) {
+    CK(cudaGetDevice(&device));
+    void* b = nullptr;
+    CK(cudaMalloc(&b, bytes + 2 * kGuardBytes));
+    base = static_cast<unsigned char*>(b);
+    p = base + kGuardBytes;
+    // the zones must hold the pattern before any stream writes: fill them on a
+    // private non-blocking stream and wait for it (not a device-wide sync,
+    // which another member thread's CUDA-graph capture would reject)
+    cudaStream_t fs = nullptr;
+    CK(cudaStreamCreateWithFlags(&fs, cudaStreamNonBlocking));
+    const cudaError_t e1 = cudaMemsetAsync(base, kGuardByte, kGuardBytes, fs);
+    const cudaError_t e2 = cudaMemsetAsync(base + kGuardBytes + bytes, kGuardByte, kGuardBytes, fs);
+    const cudaError_t e3 = cudaStreamSynchronize(fs);
+    cudaStreamDestroy(fs);
+    CK(e1);
+    CK(e2);
+    CK(e3);
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    guard_registry().insert(this);
+}
+
+void DevBuf::release() {
+    if (base) {
+        {
+            std::lock_guard<std::mutex> lk(g_guard_mu);
+            guard_registry().erase(this);
+        }
+        cudaFree(base);
+    } else if (p) {
+        cudaFree(p);
+    }
+    p = nullptr;
+    base = nullptr;
+    cap = 0;
+}
+
+void guard_check(const char* entry) {
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    int prev = 0;
+    CK(cudaGetDevice(&prev));
+    std::vector<unsigned char> h(kGuardBytes);
+    std::set<int> synced;
+    for (DevBuf* b : guard_registry()) {
+        if (!synced.count(b->device)) {
+            CK(cudaSetDevice(b->device));
+            CK(cudaDeviceSynchronize());
+            synced.insert(b->device);
+        }
+        CK(cudaSetDevice(b->device));
+        for (int side = 0; side < 2; ++side) {
+            const unsigned char* z = side == 0 ? b->base : b->base + kGuardBytes + b->cap;
+            CK(cudaMemcpy(h.data(), z, kGuardBytes, cudaMemcpyDeviceToHost));
+            for (size_t i = 0; i < kGuardBytes; ++i) {
+                if (h[i] != kGuardByte) {
+                    // re-arm the zone: the violation is reported once, by this call
+                    cudaMemset(const_cast<unsigned char*>(z), kGuardByte, kGuardBytes);
+                    cudaDeviceSynchronize();
+                    cudaSetDevice(prev);
+                    std::ostringstream os;
+                    os << entry << ": device buffer overrun — guard zone " << (side == 0 ? "before" : "after")
+                       << " a " << b->cap << "-byte buffer on device " << b->device << " overwritten at byte "
+                       << (side == 0 ? static_cast<long long>(i) - static_cast<long long>(kGuardBytes)
+                                     : static_cast<long long>(b->cap + i));
+                    raise(SMC_ERUNTIME, os.str());
+                }
+            }
+        }
+    }
+    CK(cudaSetDevice(prev));
+}
 
 
 void count_launches(smc_ctx* ctx, int64_t n) {
@@ -578,6 +670,18 @@ smc_status smc_fp32_peak(smc_ctx* ctx, double ms, double* tflops) {
 
 smc_status smc_fp64_peak(smc_ctx* ctx, double ms, double* tflops) {
     return guarded(__func__, [&] { *tflops = fma_peak(ctx, ms, true); });
+}
+
+smc_status smc_guard_selftest(smc_ctx* ctx, int64_t offset, int64_t nbytes) {
+    return guarded(__func__, [&] {
+        if (!guard_mode()) raise(SMC_EINVAL, "smc_guard_selftest: guard mode is off (set SMC_GUARD=1)");
+        if (nbytes < 0 || offset < -static_cast<int64_t>(kGuardBytes) ||
+            offset + nbytes > static_cast<int64_t>(1024 + kGuardBytes))
+            raise(SMC_EINVAL, "smc_guard_selftest: the write must stay within the guard zones");
+        CK(cudaSetDevice(ctx->device));
+        unsigned char* b = ctx->guard_probe.get<unsigned char>(1024);
+        CK(cudaMemsetAsync(b + offset, 0, static_cast<size_t>(nbytes), ctx->stream));
+    });
 }
 
 smc_status smc_bvp_observe(smc_ctx* ctx, const smc_bvp_problem* p, uint64_t seed, smc_estimate* out) {

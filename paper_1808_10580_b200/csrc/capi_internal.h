@@ -44,11 +44,20 @@ struct NvtxRange {
     NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
+// Guard zones (SMC_GUARD=1; the pool refuses compute-sanitizer): every device
+// buffer is allocated with kGuardBytes of a fixed byte pattern before and
+// after it, and every C-ABI entry ends by synchronising and checking every
+// live buffer's zones — a kernel or copy that writes past either end of its
+// buffer (up to 4 KB) fails that call with SMC_ERUNTIME naming the entry.
+bool guard_mode();
+void guard_check(const char* entry);
+
 template <class F>
 smc_status guarded(const char* name, F&& f) {
     NvtxRange range(name);
     try {
         f();
+        if (guard_mode()) guard_check(name);
         return SMC_OK;
     } catch (const Error& e) {
         g_err = e.msg;
@@ -65,9 +74,14 @@ smc_status guarded(const char* name, F&& f) {
 // Device / pinned buffers that grow on demand and are reused across calls.
 // RAII and non-copyable: a context's buffers are all released by its
 // destructor, so a new buffer cannot be forgotten in smc_destroy.
+constexpr size_t kGuardBytes = 4096;
+constexpr unsigned char kGuardByte = 0xA5;
+
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
+    unsigned char* base = nullptr;  // guard mode: the allocation, p = base + kGuardBytes
+    int device = 0;
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
@@ -76,19 +90,18 @@ struct DevBuf {
     T* get(size_t n) {
         const size_t bytes = std::max<size_t>(n * sizeof(T), 16);
         if (bytes > cap) {
-            if (p) cudaFree(p);
-            p = nullptr;
-            cap = 0;
-            CK(cudaMalloc(&p, bytes));
+            release();
+            if (guard_mode()) {
+                allocate_guarded(bytes);
+            } else {
+                CK(cudaMalloc(&p, bytes));
+            }
             cap = bytes;
         }
         return static_cast<T*>(p);
     }
-    void release() {
-        if (p) cudaFree(p);
-        p = nullptr;
-        cap = 0;
-    }
+    void allocate_guarded(size_t bytes);  // capi.cu
+    void release();
 };
 
 struct PinnedBuf {
@@ -169,6 +182,7 @@ struct smc_ctx {
     cudaEvent_t ev[4] = {};
     DevBuf image, values, aux, flags, flags2, scratch, sums, means, sumsq, sumaux, est, counts, tmp_a, tmp_b, tmp_c;
     DevBuf chunk_tmp;  // compaction scan scratch of smc_bvp_forcing_basis
+    DevBuf guard_probe;  // smc_guard_selftest
     DevBuf gx_a, gx_b, gx_c, gx_d;  // group exchange buffers (every rank's contribution)
     DevBuf pk_ip, pk_im, pk_kp, pk_km, pk_ms, pk_u, pk_blocks, pk_bad;  // device u -> field packing
     DevBuf gal_A, gal_t0, gal_t1, gal_k1, gal_k2, gal_obs, gal_grid;  // Galerkin reference solver

@@ -4,6 +4,8 @@
 #include <exception>
 #include <thread>
 
+#include <deque>
+
 #include "capi_internal.h"
 
 using namespace smc;
@@ -256,20 +258,12 @@ void pcn_chains_impl(smc_ctx* ctx, const smc_ad_problem* forward, const smc_prio
     if (!prior_only && p.n_obs > 65535)
         raise(SMC_ERUNTIME, "smc_pcn_chains: at most 65535 observations in the likelihood's forward map");
 
-    // device buffers (freed at the end of the call)
-    std::vector<void*> owned;
-    auto dalloc = [&](size_t bytes) {
-        void* q = nullptr;
-        CK(cudaMalloc(&q, std::max<size_t>(bytes, 16)));
-        owned.push_back(q);
-        return q;
+    // device buffers (RAII: freed at the end of the call, guard zones under SMC_GUARD)
+    std::deque<DevBuf> owned;
+    auto dalloc = [&](size_t bytes) -> void* {
+        owned.emplace_back();
+        return owned.back().get<unsigned char>(bytes);
     };
-    struct Freer {
-        std::vector<void*>* v;
-        ~Freer() {
-            for (void* q : *v) cudaFree(q);
-        }
-    } freer{&owned};
     auto h2d = [&](void* dst, const void* src, size_t bytes) {
         CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
     };
