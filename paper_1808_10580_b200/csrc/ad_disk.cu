@@ -26,6 +26,11 @@ namespace {
 
 constexpr int kBlock = 128;
 
+// Resident 128-thread blocks per SM for the tiled disk kernels (K > kDiskMaxK).
+#ifndef SMC_TILED_MINB
+#define SMC_TILED_MINB 4
+#endif
+
 using namespace disk;
 
 // FP32 with one particle per thread stages the packed FFMA2 block
@@ -70,7 +75,8 @@ __global__ void __launch_bounds__(kBlock, MINB) ad_particles_disk(const AdLaunch
     with_smem_coef<K, T, P>(staged, [&](const auto& C) {
         ad_particles_p<T, P>(L, obs, sample, local, span,
                              [&](const T (&x1)[P], const T (&x2)[P], T (&v1)[P], T (&v2)[P], int) {
-                                 velocity_disk<K, T, P>(C, x1, x2, v1, v2);
+                                 if constexpr (P == 1) velocity_disk_any<K, T>(C, x1, x2, v1, v2);
+                                 else velocity_disk<K, T, P>(C, x1, x2, v1, v2);
                              });
     });
 }
@@ -103,7 +109,7 @@ __global__ void __launch_bounds__(kBlock, MINB) ad_particles_disk_flat(const AdL
     with_smem_coef<K, T, 1>(staged + (sample - s0) * NS, [&](const auto& C) {
         ad_particles_p<T, 1>(L, obs, sample, local, span,
                              [&](const T (&x1)[1], const T (&x2)[1], T (&v1)[1], T (&v2)[1], int) {
-                                 velocity_disk<K, T, 1>(C, x1, x2, v1, v2);
+                                 velocity_disk_any<K, T>(C, x1, x2, v1, v2);
                              });
     });
 }
@@ -145,7 +151,7 @@ __global__ void __launch_bounds__(kBlock, MINB)
                                  velocity_disk<K, T, 1>(C, x1, x2, v1, v2);
                              } else {
                                  const ParamCoef<K, T> C{P, zero};
-                                 velocity_disk<K, T, 1>(C, x1, x2, v1, v2);
+                                 velocity_disk_any<K, T>(C, x1, x2, v1, v2);
                              }
                          };
     // FP32 takes the Philox round keys from the parameter bank too; FP64 does
@@ -179,7 +185,7 @@ cudaError_t launch_param(const AdLaunch& L, cudaStream_t s) {
                     static_cast<unsigned>(L.unit_cpo > 0 ? 1 : L.n_obs), 1);
     AdLaunch LK = L;
     LK.rk = make_round_keys(L.seed);
-    ad_particles_disk_param<K, T, (K <= 8 ? 4 : 3)><<<grid, kBlock, 0, s>>>(LK, P);
+    ad_particles_disk_param<K, T, (K <= 8 ? 4 : (K <= kDiskMaxK ? 3 : SMC_TILED_MINB))><<<grid, kBlock, 0, s>>>(LK, P);
     return cudaGetLastError();
 }
 
@@ -198,7 +204,11 @@ cudaError_t dispatch_param(const AdLaunch& L, int K, cudaStream_t s) {
         case 10: return launch_param<10, T>(L, s);
         case 11: return launch_param<11, T>(L, s);
         case 12: return launch_param<12, T>(L, s);
-        default: return cudaErrorNotSupported;
+        default:
+            if constexpr (std::is_same<T, double>::value) {
+                if (K == 25) return launch_param<25, T>(L, s);
+            }
+            return cudaErrorNotSupported;
     }
 }
 
@@ -229,7 +239,7 @@ cudaError_t launch_k(const AdLaunch& L, const double* coef, cudaStream_t s) {
 // per thread need ~250 registers.
 template <int K, int P>
 struct MinBlocks {
-    static constexpr int value = P == 2 ? 2 : (K <= 8 ? 4 : 3);
+    static constexpr int value = P == 2 ? 2 : (K <= 8 ? 4 : (K <= kDiskMaxK ? 3 : SMC_TILED_MINB));
 };
 
 template <class T, int P>
@@ -247,7 +257,11 @@ cudaError_t dispatch_p(const AdLaunch& L, int K, const double* c, cudaStream_t s
         case 10: return launch_k<10, T, P, MinBlocks<10, P>::value>(L, c, s);
         case 11: return launch_k<11, T, P, MinBlocks<11, P>::value>(L, c, s);
         case 12: return launch_k<12, T, P, MinBlocks<12, P>::value>(L, c, s);
-        default: return cudaErrorNotSupported;
+        default:
+            if constexpr (std::is_same<T, double>::value && P == 1) {
+                if (K == 25) return launch_k<25, T, 1, MinBlocks<25, 1>::value>(L, c, s);
+            }
+            return cudaErrorNotSupported;
     }
 }
 

@@ -223,8 +223,10 @@ AdImage build_ad_image(const smc_ad_problem& p, const std::vector<const Prepared
     A.order_off = im.add_vec(order);
     A.th = add_scalar(im, p.initial_condition);
     A.vr = add_velocity(im, structure, fills);
-    // Dense fields with K <= kDiskMaxK take the compile-time disk kernel.
-    const bool disk = !structure.is_constant && p.precision != SMC_FP64_STRICT && structure.K <= kDiskMaxK &&
+    // Dense fields with a compile-time disk kernel for their K take it
+    // (K <= kDiskMaxK; FP64 also the tiled disk kernels' K).
+    const bool disk = !structure.is_constant && p.precision != SMC_FP64_STRICT &&
+                      disk_kernel_for(structure.K, p.precision == SMC_FP64) &&
                       2 * structure.modes.size() >= static_cast<size_t>(disk_n_modes(structure.K)) &&
                       std::getenv("SMC_DISABLE_DISK") == nullptr;
     if (disk) {

@@ -250,7 +250,8 @@ void pcn_chains_impl(smc_ctx* ctx, const smc_ad_problem* forward, const smc_prio
     // lattice structure of the full prior disk and the u -> block gather map
     // (disk layout for K <= kDiskMaxK, tiled lattice otherwise)
     const PreparedVelocity structure = prior_structure(prior->cutoff);
-    const bool use_disk = prior->cutoff <= kDiskMaxK && std::getenv("SMC_DISABLE_DISK") == nullptr;
+    const bool use_disk =
+        disk_kernel_for(prior->cutoff, p.precision == SMC_FP64) && std::getenv("SMC_DISABLE_DISK") == nullptr;
     const LatticeHost Lh = lattice_structure(structure);
     const PackMap pmap = pack_map(prior->cutoff, use_disk, &Lh);
     const int64_t stride = pmap.stride;

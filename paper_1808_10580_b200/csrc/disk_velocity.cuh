@@ -389,5 +389,146 @@ __device__ __forceinline__ void velocity_disk(const CA& C, const T (&x1)[P], con
     }
 }
 
+// ---------------------------------------------------------------------------
+// Tiled disk series for kDiskMaxK < K (FP64 K1; disk_tiled_instantiated():
+// the batched C4 prior has K = 25, M = 980).  Powers for every j no longer
+// fit in registers, so the columns run in tiles of 8 (P2[j], Q[j] of one tile
+// in registers, continued by complex products from the previous tile), and
+// inside a tile every row k1 with modes there unrolls exactly its pairs —
+// the shape is known at compile time, so unlike the generic tiled kernel
+// (velocity.cuh) no pair slot is padding, no coefficient address is
+// computed at run time and the loop has no trip counts.  Same disk_shape.h
+// coefficient layout as the K <= 12 kernel.  Per (tile, row): P1 <- P1 e1
+// (restarted each tile) and the fold v2 += k1 Re(P1 A), v1 -= Re(P1 B').
+// Measured and rejected: interleaving the pair updates of two rows (eight
+// accumulator chains instead of four): C4 2974 -> 3032 ms.
+constexpr int kDiskTile = 8;
+
+template <int K, int T0>
+struct DiskTile {
+    static constexpr int j0 = kDiskTile * T0;
+    static constexpr int w = (K - j0) < kDiskTile ? (K - j0) : kDiskTile;  // columns (row 0 reaches j = K)
+    static constexpr int npair(int k1) {
+        const int e = DiskShape<K>::jmax(k1) - j0;
+        return e < 0 ? 0 : (e > kDiskTile ? kDiskTile : e);
+    }
+    static constexpr int rows() {  // k1 = 1..rows() have pairs here (jmax is non-increasing in k1)
+        if (T0 == 0) return K;     // tile 0 also carries every row's (k1, 0) mode
+        int r = 0;
+        while (r < K && DiskShape<K>::jmax(r + 1) > j0) ++r;
+        return r;
+    }
+};
+
+template <int K>
+constexpr int kDiskTiles = (K + kDiskTile - 1) / kDiskTile;
+
+template <class T>
+struct TilePowers {
+    T pr[kDiskTile], pi[kDiskTile], qr[kDiskTile], qi[kDiskTile];
+};
+
+template <int K, int T0, int K1, int Q, class T, class CA>
+__device__ __forceinline__ void tiled_pair(const CA& C, const TilePowers<T>& W, T& Ar, T& Ai, T& Br, T& Bi) {
+    constexpr int o = 4 * (DiskShape<K>::pair_offset(K1) + DiskTile<K, T0>::j0 + Q);
+    T ar, ai, br, bi;
+    get4<o>(C, ar, ai, br, bi);
+    Ar = fma(ar, W.pr[Q], Ar);
+    Ai = fma(ai, W.pr[Q], Ai);
+    Br = fma(br, W.qr[Q], Br);
+    Bi = fma(bi, W.qr[Q], Bi);
+    Ar = fma(bi, -W.pi[Q], Ar);
+    Ai = fma(br, W.pi[Q], Ai);
+    Br = fma(ai, -W.qi[Q], Br);
+    Bi = fma(ar, W.qi[Q], Bi);
+}
+
+template <int K, int T0, int K1, class T, class CA, int... Qs>
+__device__ __forceinline__ void tiled_pairs(const CA& C, const TilePowers<T>& W, T& Ar, T& Ai, T& Br, T& Bi,
+                                            std::integer_sequence<int, Qs...>) {
+    (tiled_pair<K, T0, K1, Qs>(C, W, Ar, Ai, Br, Bi), ...);
+}
+
+template <int K, int T0, int K1, class T, class CA>
+__device__ __forceinline__ void tiled_row(const CA& C, const TilePowers<T>& W, T c1, T s1, T& p1r, T& p1i, T& acc1,
+                                          T& acc2) {
+    if constexpr (K1 > 1) {
+        const T nr = fma(p1r, c1, -p1i * s1);
+        p1i = fma(p1r, s1, p1i * c1);
+        p1r = nr;
+    }
+    T Ar = T(0), Ai = T(0), Br = T(0), Bi = T(0);
+    if constexpr (T0 == 0) C.template get2<DiskShape<K>::g0_offset + 2 * (K1 - 1)>(Ar, Ai);
+    tiled_pairs<K, T0, K1>(C, W, Ar, Ai, Br, Bi, std::make_integer_sequence<int, DiskTile<K, T0>::npair(K1)>{});
+    acc2 = fma(T(K1), fma(p1r, Ar, -p1i * Ai), acc2);
+    acc1 = fma(-p1r, Br, fma(p1i, Bi, acc1));
+}
+
+template <int K, int T0, class T, class CA, int... K1s>
+__device__ __forceinline__ void tiled_rows(const CA& C, const TilePowers<T>& W, T c1, T s1, T& acc1, T& acc2,
+                                           std::integer_sequence<int, K1s...>) {
+    T p1r = c1, p1i = s1;
+    (tiled_row<K, T0, K1s + 1>(C, W, c1, s1, p1r, p1i, acc1, acc2), ...);
+}
+
+template <int K, int T0, int Q, class T, class CA>
+__device__ __forceinline__ void tiled_row0_term(const CA& C, const TilePowers<T>& W, T& a0, T& a1) {
+    T gr, gi;
+    C.template get2<DiskShape<K>::row0_offset + 2 * (DiskTile<K, T0>::j0 + Q)>(gr, gi);
+    a0 = fma(gr, -W.qr[Q], a0);
+    a1 = fma(gi, W.qi[Q], a1);
+}
+
+template <int K, int T0, class T, class CA, int... Qs>
+__device__ __forceinline__ void tiled_row0(const CA& C, const TilePowers<T>& W, T& a0, T& a1,
+                                           std::integer_sequence<int, Qs...>) {
+    (tiled_row0_term<K, T0, Qs>(C, W, a0, a1), ...);
+}
+
+template <int K, int T0, class T, class CA>
+__device__ __forceinline__ void tiled_tile(const CA& C, T c1, T s1, T c2, T s2, T& p2r, T& p2i, T& a0, T& a1,
+                                           T& acc1, T& acc2) {
+    using Tl = DiskTile<K, T0>;
+    TilePowers<T> W;
+#pragma unroll
+    for (int q = 0; q < Tl::w; ++q) {  // P2[j0 + q + 1] = P2[j0 + q] e2
+        const T nr = fma(p2r, c2, -p2i * s2);
+        p2i = fma(p2r, s2, p2i * c2);
+        p2r = nr;
+        W.pr[q] = p2r;
+        W.pi[q] = p2i;
+        W.qr[q] = T(Tl::j0 + q + 1) * p2r;
+        W.qi[q] = T(Tl::j0 + q + 1) * p2i;
+    }
+    tiled_row0<K, T0>(C, W, a0, a1, std::make_integer_sequence<int, Tl::w>{});
+    tiled_rows<K, T0>(C, W, c1, s1, acc1, acc2, std::make_integer_sequence<int, Tl::rows()>{});
+}
+
+template <int K, class T, class CA, int... Ts>
+__device__ __forceinline__ void tiled_tiles(const CA& C, T c1, T s1, T c2, T s2, T& a0, T& a1, T& acc1, T& acc2,
+                                            std::integer_sequence<int, Ts...>) {
+    T p2r = T(1), p2i = T(0);
+    (tiled_tile<K, Ts>(C, c1, s1, c2, s2, p2r, p2i, a0, a1, acc1, acc2), ...);
+}
+
+template <int K, class T, class CA>
+__device__ __forceinline__ void velocity_disk_tiled(const CA& C, T x1, T x2, T& v1, T& v2) {
+    T s1, c1, s2, c2;
+    sincospi_t(T(2) * x1, &s1, &c1);
+    sincospi_t(T(2) * x2, &s2, &c2);
+    T a0 = T(0), a1 = T(0), acc1 = T(0), acc2 = T(0);
+    tiled_tiles<K>(C, c1, s1, c2, s2, a0, a1, acc1, acc2, std::make_integer_sequence<int, kDiskTiles<K>>{});
+    v1 = acc1 + (a0 + a1);
+    v2 = acc2;
+}
+
+// Either disk form for P = 1.
+template <int K, class T, class CA>
+__device__ __forceinline__ void velocity_disk_any(const CA& C, const T (&x1)[1], const T (&x2)[1], T (&v1)[1],
+                                                  T (&v2)[1]) {
+    if constexpr (K > kDiskMaxK) velocity_disk_tiled<K, T>(C, x1[0], x2[0], v1[0], v2[0]);
+    else velocity_disk<K, T, 1>(C, x1, x2, v1, v2);
+}
+
 }  // namespace disk
 }  // namespace smc
