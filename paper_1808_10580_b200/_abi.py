@@ -193,6 +193,8 @@ def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
             "`python -c 'import __graft_entry__ as g; g.build()'` (there is no CPU fallback)")
     lib = C.CDLL(str(p))
     for name, (res, args) in _PROTOS.items():
+        if os.environ.get("SMC_LIBRARY") and not hasattr(lib, name):
+            continue  # an older A/B build without this entry point
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
