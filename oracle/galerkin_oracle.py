@@ -1,12 +1,14 @@
 """numpy restatement of the reference's spectral Galerkin solver
 (TEST INFRASTRUCTURE ONLY — the checker for smc_galerkin_*).
 
-galerkin.cpp needs Eigen, which is absent here, so the reference itself
-cannot be built; this restatement follows src/galerkin.cpp line by line
-(cited per function) with numpy complex128 in place of Eigen::MatrixXcd,
-and is pinned independently by closed forms (tests/test_galerkin_oracle.py):
-the heat equation and any constant velocity make A diagonal, so explicit
-Euler gives Theta_l(t) = Theta_l(0) prod_i (1 + dt_i A_ll) exactly.
+This restatement follows src/galerkin.cpp line by line (cited per function)
+with numpy complex128 in place of Eigen::MatrixXcd.  It is pinned two ways
+(tests/test_galerkin_oracle.py): by closed forms (the heat equation and any
+constant velocity make A diagonal, so explicit Euler gives
+Theta_l(t) = Theta_l(0) prod_i (1 + dt_i A_ll) exactly), and against the
+reference's own galerkin.cpp, which oracle/Makefile compiles into
+oracle/_ref against oracle/eigen_shim/Eigen/Dense (a restatement of the
+small dense Eigen subset it uses; Eigen itself is absent here).
 """
 from __future__ import annotations
 

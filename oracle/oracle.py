@@ -271,6 +271,53 @@ class Reference(_Checker):
         _status(self.lib, self.prefix, rc)
         return {"argmin": arg, "min_value": sc[0], "iterations": int(sc[1]), "stop_reason": reason.value.decode()}
 
+    # ---- spectral Galerkin reference solver: the reference's src/galerkin.cpp
+    # compiled against oracle/eigen_shim (its Eigen dependency is absent) ----
+    @staticmethod
+    def _gbasis(kind: str, L: int):
+        return A.smc_galerkin_basis(1 if kind == "disk" else 0, int(L))
+
+    def galerkin_spectral_radius(self, spec, kind: str, L: int) -> float:
+        p, keep = spec._pod()
+        out = C.c_double()
+        rc = self.lib.ref_galerkin_spectral_radius(C.byref(p), C.byref(self._gbasis(kind, L)), C.byref(out))
+        _status(self.lib, self.prefix, rc)
+        return out.value
+
+    def galerkin_solve_ad(self, spec, kind: str, L: int, dt_ref: float) -> dict:
+        """-> {observation_values, coefficients_at_observations [n_obs][nb]
+        (complex), final_coefficients [nb], basis_modes, dt_used, steps}."""
+        p, keep = spec._pod()
+        cap = (2 * L + 1) ** 2
+        n_obs = len(spec.observations)
+        vals = np.zeros(n_obs)
+        cat = np.zeros((n_obs, cap, 2))
+        fin = np.zeros((cap, 2))
+        modes = np.zeros((cap, 2), dtype=np.int32)
+        r = A.smc_galerkin_result(vals.ctypes.data_as(_dp), cat.ctypes.data_as(_dp), fin.ctypes.data_as(_dp), 0.0, 0)
+        self.lib.ref_galerkin_solve_ad.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p,
+                                                   C.c_int64]
+        rc = self.lib.ref_galerkin_solve_ad(C.byref(p), C.byref(self._gbasis(kind, L)), C.c_double(dt_ref),
+                                            C.byref(r), modes.ctypes.data, C.c_int64(cap))
+        _status(self.lib, self.prefix, rc)
+        # the basis size: box (2L+1)^2, disk counted like basis_mode_list
+        nb = cap if kind == "box" else sum(1 for a in range(-L, L + 1) for b in range(-L, L + 1) if a * a + b * b <= L * L)
+        # coefficients_at_observations was written with stride nb
+        flat = cat.reshape(-1)[: n_obs * nb * 2].reshape(n_obs, nb, 2)
+        return {"observation_values": vals, "coefficients_at_observations": flat[..., 0] + 1j * flat[..., 1],
+                "final_coefficients": fin[:nb, 0] + 1j * fin[:nb, 1],
+                "basis_modes": [tuple(int(v) for v in m) for m in modes[:nb]], "dt_used": r.dt_used,
+                "steps": int(r.steps)}
+
+    def galerkin_field_grid(self, coefficients, modes, n: int) -> np.ndarray:
+        c = np.ascontiguousarray(np.stack([np.real(coefficients), np.imag(coefficients)], axis=-1), dtype=np.float64)
+        m = np.ascontiguousarray(np.asarray(modes, dtype=np.int32).reshape(-1, 2))
+        out = np.zeros(int(n) * int(n)) if n >= 2 else np.zeros(1)
+        self.lib.ref_galerkin_field_grid.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]
+        rc = self.lib.ref_galerkin_field_grid(len(m), m.ctypes.data, c.ctypes.data, int(n), out.ctypes.data)
+        _status(self.lib, self.prefix, rc)
+        return out
+
     def resolved_dt_ad(self, spec) -> float:
         p, keep = spec._pod()
         out = C.c_double()

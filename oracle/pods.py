@@ -225,3 +225,12 @@ def paper_bvp(n_particles: int = 16000, amplitudes=(0.0, 0.0, 0.0), observations
 def c3(n_particles: int = 1_000_000) -> BvpSpec:
     obs = [(a, b) for a in (0.1, 0.3, 0.5, 0.7, 0.9) for b in (0.1, 0.3, 0.5, 0.7, 0.9)]
     return paper_bvp(n_particles, amplitudes=(1.0, -0.5, 2.0), observations=obs)
+
+
+class smc_galerkin_basis(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("cutoff", C.c_int32)]
+
+
+class smc_galerkin_result(C.Structure):
+    _fields_ = [("observation_values", C.POINTER(C.c_double)), ("coefficients_at_observations", C.POINTER(C.c_double)),
+                ("final_coefficients", C.POINTER(C.c_double)), ("dt_used", C.c_double), ("steps", C.c_int64)]

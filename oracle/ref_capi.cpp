@@ -9,6 +9,7 @@
 // reference's public API, so that tests/ and bench.py (cpu_baseline and
 // --impl reference) can run the unmodified reference on the same inputs as the
 // CUDA path.  The product never links this file.
+#include <algorithm>
 #include <cmath>
 #include <complex>
 #include <cstdint>
@@ -24,6 +25,7 @@
 #include "scalarmc/fields.hpp"
 #include "scalarmc/forward_ad.hpp"
 #include "scalarmc/forward_bvp.hpp"
+#include "scalarmc/galerkin.hpp"
 #include "scalarmc/geometry.hpp"
 #include "scalarmc/inference.hpp"
 #include "scalarmc/optimize.hpp"
@@ -388,5 +390,59 @@ int ref_optimize_forcing(const smc_bvp_problem* base, int64_t n_bumps, const dou
 }
 
 int ref_resolve_workers(int requested) { return resolve_workers(requested); }
+
+// ---- spectral Galerkin reference solver (src/galerkin.cpp, built against
+// eigen_shim/Eigen/Dense) --------------------------------------------------
+static GalerkinBasis to_basis(const smc_galerkin_basis& b) {
+    return GalerkinBasis{b.kind == 1 ? GalerkinBasis::Kind::disk : GalerkinBasis::Kind::box, b.cutoff};
+}
+
+int ref_galerkin_spectral_radius(const smc_ad_problem* p, const smc_galerkin_basis* b, double* out) {
+    return guarded([&] { *out = galerkin_spectral_radius(to_ad(*p), to_basis(*b)); });
+}
+
+// out->observation_values [n_obs]; out->coefficients_at_observations
+// [n_obs][nb][2] and out->final_coefficients [nb][2] when non-null; modes
+// [nb][2] when non-null (capacity nb_cap modes).
+int ref_galerkin_solve_ad(const smc_ad_problem* p, const smc_galerkin_basis* b, double dt_ref,
+                          smc_galerkin_result* out, int32_t* modes, int64_t nb_cap) {
+    return guarded([&] {
+        const GalerkinResult r = galerkin_solve_ad(to_ad(*p), to_basis(*b), dt_ref);
+        const std::size_t nb = r.basis_modes.size();
+        if (static_cast<int64_t>(nb) > nb_cap) throw std::out_of_range("ref_galerkin_solve_ad: mode capacity");
+        for (std::size_t j = 0; j < r.observation_values.size(); ++j) out->observation_values[j] = r.observation_values[j];
+        if (out->coefficients_at_observations)
+            for (std::size_t j = 0; j < r.coefficients_at_observations.size(); ++j)
+                for (std::size_t l = 0; l < nb; ++l) {
+                    out->coefficients_at_observations[2 * (j * nb + l)] = r.coefficients_at_observations[j][l].real();
+                    out->coefficients_at_observations[2 * (j * nb + l) + 1] = r.coefficients_at_observations[j][l].imag();
+                }
+        if (out->final_coefficients)
+            for (std::size_t l = 0; l < nb; ++l) {
+                out->final_coefficients[2 * l] = r.final_coefficients[l].real();
+                out->final_coefficients[2 * l + 1] = r.final_coefficients[l].imag();
+            }
+        if (modes)
+            for (std::size_t l = 0; l < nb; ++l) {
+                modes[2 * l] = r.basis_modes[l].first;
+                modes[2 * l + 1] = r.basis_modes[l].second;
+            }
+        out->dt_used = r.dt_used;
+        out->steps = r.steps;
+    });
+}
+
+int ref_galerkin_field_grid(int64_t nb, const int32_t* modes, const double* coefficients, int32_t n,
+                            double* grid) {
+    return guarded([&] {
+        GalerkinResult r;
+        for (int64_t l = 0; l < nb; ++l) {
+            r.basis_modes.emplace_back(modes[2 * l], modes[2 * l + 1]);
+            r.final_coefficients.emplace_back(coefficients[2 * l], coefficients[2 * l + 1]);
+        }
+        const std::vector<double> g = galerkin_field_grid(r, n);
+        std::copy(g.begin(), g.end(), grid);
+    });
+}
 
 }  // extern "C"

@@ -64,3 +64,50 @@ def test_basis_modes():
         G.basis_modes("box", 0)
     assert S.GalerkinBasis("disk", 5).modes() == G.basis_modes("disk", 5)
     assert S.GalerkinBasis("box", 4).modes() == G.basis_modes("box", 4)
+
+
+# ---- the reference's own galerkin.cpp (compiled against oracle/eigen_shim) ----
+def _fourier(K=3, seed=4, scale=0.3):
+    import specs
+    f = specs.random_fourier(np.random.default_rng(seed), 6, K)
+    modes = [S.VelocityMode(int(k1), int(k2), complex(scale * re, scale * im))
+             for (k1, k2), (re, im) in zip(f.k.tolist(), f.coeff.tolist())]
+    return S.VelocityField.fourier(S.FourierVelocityField(modes, K))
+
+
+REF_CASES = {
+    "fourier_box": (lambda: _fourier(), "box", 5, [(1.0, (2 * math.pi, 0.0), 0.0), (0.6, (0.0, 2 * math.pi), 0.7)]),
+    "fourier_disk": (lambda: _fourier(K=2, seed=9), "disk", 6, [(0.4, (2 * math.pi, 2 * math.pi), -0.3)]),
+    "constant_box": (lambda: S.VelocityField.constant((0.8, -0.3)), "box", 4, [(1.0, (2 * math.pi, 0.0), 0.2)]),
+}
+
+
+@pytest.mark.parametrize("name", list(REF_CASES))
+def test_restatement_matches_compiled_reference(reference, name):
+    """The numpy restatement against the reference's galerkin.cpp itself:
+    same basis order, step count, observation values and coefficients (to
+    rounding: the shim's GEMV and numpy sum in different orders)."""
+    make, kind, L, terms = REF_CASES[name]
+    sp = spec(make(), 0.02, terms, [(0.02, (0.5, 0.5)), (0.0437, (0.25, 0.75)), (0.01, (0.9, 0.3))])
+    A = G.assemble(sp.velocity, 0.02, G.basis_modes(kind, L))
+    radius = np.abs(A).sum(axis=1).max()
+    assert abs(reference.galerkin_spectral_radius(sp, kind, L) - radius) <= 1e-13 * radius
+    dt = min(2e-4, 1.0 / radius)
+    want = reference.galerkin_solve_ad(sp, kind, L, dt)
+    vals, theta, steps, modes = G.solve(sp, kind, L, dt)
+    assert want["basis_modes"] == modes and want["steps"] == steps and want["dt_used"] == dt
+    assert np.max(np.abs(want["observation_values"] - vals)) <= 1e-12 * max(1.0, np.max(np.abs(vals)))
+    assert np.max(np.abs(want["final_coefficients"] - theta)) <= 1e-12 * max(1.0, np.max(np.abs(theta)))
+    grid = reference.galerkin_field_grid(want["final_coefficients"], modes, 9)
+    assert np.max(np.abs(grid - G.field_grid(want["final_coefficients"], modes, 9))) <= 1e-12
+
+
+def test_compiled_reference_errors(reference):
+    sp = spec(_fourier(), 0.02, [(1.0, (2 * math.pi, 0.0), 0.0)], [(0.02, (0.5, 0.5))])
+    with pytest.raises(ValueError, match="dt_ref must be positive"):
+        reference.galerkin_solve_ad(sp, "box", 4, 0.0)
+    with pytest.raises(ValueError, match="cutoff must be >= 1"):
+        reference.galerkin_solve_ad(sp, "box", 0, 1e-3)
+    radius = reference.galerkin_spectral_radius(sp, "box", 6)
+    with pytest.raises(RuntimeError, match="violates the stability estimate; suggest dt_ref <= "):
+        reference.galerkin_solve_ad(sp, "box", 6, 3.0 / radius)

@@ -1,6 +1,8 @@
 """Device Galerkin reference solver (smc_galerkin_*)
-against the numpy restatement of src/galerkin.cpp (oracle/galerkin_oracle.py,
-pinned by closed forms in tests/test_galerkin_oracle.py) and against the
+against the reference's own src/galerkin.cpp (compiled into oracle/_ref
+against oracle/eigen_shim, its absent Eigen dependency restated), against the
+numpy restatement (oracle/galerkin_oracle.py, pinned by closed forms and by
+the compiled reference in tests/test_galerkin_oracle.py) and against the
 particle forward map (the paper's Fig. 8 comparison)."""
 import math
 
@@ -56,6 +58,26 @@ def test_matches_oracle(ctx, name):
     assert np.max(np.abs(res.final_coefficients - theta)) <= 1e-10 * max(1.0, np.max(np.abs(theta)))
     last = int(np.argmax([o.t for o in spec.observations]))
     assert np.max(np.abs(res.coefficients_at_observations[last] - res.final_coefficients)) == 0.0
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_matches_compiled_reference(ctx, reference, name):
+    make, kind, L, cap = CASES[name]
+    spec = make()
+    dt = stable_dt(spec, kind, L, cap)
+    res = S.galerkin_solve_ad(spec, S.GalerkinBasis(kind, L), dt, keep_observation_coefficients=True, ctx=ctx)
+    want = reference.galerkin_solve_ad(spec, kind, L, dt)
+    assert res.steps == want["steps"] and res.dt_used == want["dt_used"] and res.basis_modes == want["basis_modes"]
+    vals = want["observation_values"]
+    assert np.max(np.abs(res.observation_values - vals)) <= 1e-10 * max(1.0, np.max(np.abs(vals)))
+    th = want["final_coefficients"]
+    assert np.max(np.abs(res.final_coefficients - th)) <= 1e-10 * max(1.0, np.max(np.abs(th)))
+    cat = want["coefficients_at_observations"]
+    assert np.max(np.abs(res.coefficients_at_observations - cat)) <= 1e-10 * max(1.0, np.max(np.abs(cat)))
+    radius = S.galerkin_spectral_radius(spec, S.GalerkinBasis(kind, L), ctx=ctx)
+    assert abs(radius - reference.galerkin_spectral_radius(spec, kind, L)) <= 1e-12 * radius
+    grid = S.galerkin_field_grid(res, 11, ctx=ctx)
+    assert np.max(np.abs(grid - reference.galerkin_field_grid(res.final_coefficients, res.basis_modes, 11))) < 1e-11
 
 
 def test_field_grid(ctx):
