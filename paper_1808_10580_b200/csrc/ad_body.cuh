@@ -24,7 +24,7 @@ __device__ __forceinline__ float log_t(float x) { return __logf(x); }
 // computed on a clamped index and not stored.  RK: the launch carries the
 // Philox round keys of L.seed (L.rk; single-sample launches without per-sample
 // seeds).
-template <class T, int P, class Vel, bool RK = false>
+template <class T, int P, class Vel, bool RK = false, bool UNIT = true>
 __device__ __forceinline__ void ad_particles_p(const AdLaunch& L, int obs, int sample, const int64_t (&local)[P],
                                                int64_t span, Vel&& velocity) {
     const AdObsImg o = L.obs[obs];
@@ -83,21 +83,24 @@ __device__ __forceinline__ void ad_particles_p(const AdLaunch& L, int obs, int s
             x2[p] -= floor(x2[p]);
         }
     }
-    double* out = ad_out_row(L, sample, obs, span);
+    // UNIT = false: a launch that is never in unit mode (its output row
+    // needs no runtime mode check)
+    double* out = UNIT ? ad_out_row(L, sample, obs, span)
+                       : L.values + (static_cast<int64_t>(sample) * L.n_obs + obs) * span;
 #pragma unroll
     for (int p = 0; p < P; ++p)
         if (local[p] < span) out[local[p]] = scalar_eval(L.theta0, double(x1[p]), double(x2[p]));
 }
 
 // Single-particle convenience wrapper.
-template <class T, class Vel>
+template <class T, bool UNIT = true, class Vel>
 __device__ __forceinline__ void ad_particle(const AdLaunch& L, int obs, int sample, int64_t local, int64_t span,
                                             Vel&& velocity) {
     const int64_t loc[1] = {local};
-    ad_particles_p<T, 1>(L, obs, sample, loc, span,
-                         [&](const T (&x1)[1], const T (&x2)[1], T (&v1)[1], T (&v2)[1], int) {
-                             velocity(x1[0], x2[0], v1[0], v2[0]);
-                         });
+    auto vel = [&](const T (&x1)[1], const T (&x2)[1], T (&v1)[1], T (&v2)[1], int) {
+        velocity(x1[0], x2[0], v1[0], v2[0]);
+    };
+    ad_particles_p<T, 1, decltype(vel)&, false, UNIT>(L, obs, sample, loc, span, vel);
 }
 
 }  // namespace smc

@@ -73,11 +73,11 @@ __global__ void __launch_bounds__(kBlock, MINB) ad_particles_disk(const AdLaunch
 #pragma unroll
     for (int p = 0; p < P; ++p) local[p] = base + static_cast<int64_t>(p) * kBlock;
     with_smem_coef<K, T, P>(staged, [&](const auto& C) {
-        ad_particles_p<T, P>(L, obs, sample, local, span,
-                             [&](const T (&x1)[P], const T (&x2)[P], T (&v1)[P], T (&v2)[P], int) {
-                                 if constexpr (P == 1) velocity_disk_any<K, T>(C, x1, x2, v1, v2);
-                                 else velocity_disk<K, T, P>(C, x1, x2, v1, v2);
-                             });
+        auto vel = [&](const T (&x1)[P], const T (&x2)[P], T (&v1)[P], T (&v2)[P], int) {
+            if constexpr (P == 1) velocity_disk_any<K, T>(C, x1, x2, v1, v2);
+            else velocity_disk<K, T, P>(C, x1, x2, v1, v2);
+        };
+        ad_particles_p<T, P, decltype(vel)&, false, false>(L, obs, sample, local, span, vel);  // never unit mode
     });
 }
 
@@ -107,10 +107,10 @@ __global__ void __launch_bounds__(kBlock, MINB) ad_particles_disk_flat(const AdL
     int64_t local[1] = {flat - static_cast<int64_t>(sample) * span};
     const int obs = __ldg(L.obs_order + blockIdx.y);
     with_smem_coef<K, T, 1>(staged + (sample - s0) * NS, [&](const auto& C) {
-        ad_particles_p<T, 1>(L, obs, sample, local, span,
-                             [&](const T (&x1)[1], const T (&x2)[1], T (&v1)[1], T (&v2)[1], int) {
-                                 velocity_disk_any<K, T>(C, x1, x2, v1, v2);
-                             });
+        auto vel = [&](const T (&x1)[1], const T (&x2)[1], T (&v1)[1], T (&v2)[1], int) {
+            velocity_disk_any<K, T>(C, x1, x2, v1, v2);
+        };
+        ad_particles_p<T, 1, decltype(vel)&, false, false>(L, obs, sample, local, span, vel);  // never unit mode
     });
 }
 
@@ -285,7 +285,11 @@ cudaError_t launch_ad_disk(const AdLaunch& L, int K, const double* coef, cudaStr
     // one coefficient block with its host copy: the kernel-parameter path
     // (SMC_DISK_P=2 keeps the shared-memory kernel, which has the P=2 form)
     const char* pe = std::getenv("SMC_DISK_P");
-    if (L.n_samples == 1 && L.host_disk && !L.seeds && (L.unit_cpo > 0 || !(pe && std::atoi(pe) == 2)))
+    // The tiled disk kernels (K > kDiskMaxK) take the parameter path only in
+    // unit mode: their parameter form spills (K = 25 single sample: 80.6 ms
+    // vs 77.0 ms staged in shared memory).
+    if (L.n_samples == 1 && L.host_disk && !L.seeds &&
+        (L.unit_cpo > 0 || (K <= kDiskMaxK && !(pe && std::atoi(pe) == 2))))
         return L.precision == 1 ? dispatch_param<float>(L, K, s) : dispatch_param<double>(L, K, s);
     return L.precision == 1 ? dispatch<float>(L, K, coef, s) : dispatch<double>(L, K, coef, s);
 }

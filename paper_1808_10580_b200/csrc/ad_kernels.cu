@@ -23,7 +23,10 @@ constexpr size_t kSmemMax = 220 * 1024;    // larger tables: one 512-thread bloc
 constexpr size_t kSmemHard = 227 * 1024;
 constexpr int kMaxDevices = 64;
 
-template <class T, bool SMEM, int kBlock, bool OM>
+// UNIT: the launch is in unit mode (sharded single-sample launches,
+// kernels.h); a compile-time flag so the unsharded kernel carries none of it
+// (as a runtime branch it cost C5 7 %: 4634 -> 4966 ms).
+template <class T, bool SMEM, int kBlock, bool OM, bool UNIT>
 __global__ void __launch_bounds__(kBlock, 512 / kBlock) ad_particles(const AdLaunch L) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // OM: grid (particle blocks, samples, observations longest first);
@@ -44,12 +47,12 @@ __global__ void __launch_bounds__(kBlock, 512 / kBlock) ad_particles(const AdLau
     int64_t span = L.p_end - L.p_begin;
     if (local >= span) return;
     int ob = obs;
-    if (L.unit_cpo > 0) {  // sharded launch (kernels.h unit mode)
+    if constexpr (UNIT) {  // sharded launch (kernels.h unit mode)
         if (!unit_coords(L, local, ob, local)) return;
         span = L.n_particles;
     }
     const T c1 = T(L.vel.c1), c2 = T(L.vel.c2);
-    ad_particle<T>(L, ob, sample, local, span, [&](T x1, T x2, T& v1, T& v2) {
+    ad_particle<T, UNIT>(L, ob, sample, local, span, [&](T x1, T x2, T& v1, T& v2) {
         if (is_const) {
             v1 = c1;
             v2 = c2;
@@ -61,7 +64,7 @@ __global__ void __launch_bounds__(kBlock, 512 / kBlock) ad_particles(const AdLau
     });
 }
 
-template <class T, bool SMEM, int BS, bool OM>
+template <class T, bool SMEM, int BS, bool OM, bool UNIT>
 void go_om(const AdLaunch& L, int64_t nb, size_t smem, cudaStream_t s) {
     const dim3 grid = OM ? dim3(static_cast<unsigned>(nb), static_cast<unsigned>(L.n_samples),
                                 static_cast<unsigned>(L.n_obs))
@@ -73,20 +76,21 @@ void go_om(const AdLaunch& L, int64_t nb, size_t smem, cudaStream_t s) {
         int dev = 0;
         cudaGetDevice(&dev);
         const auto configure = [] {
-            cudaFuncSetAttribute(ad_particles<T, true, BS, OM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaFuncSetAttribute(ad_particles<T, true, BS, OM, UNIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(kSmemHard));
         };
         if (dev >= 0 && dev < kMaxDevices) std::call_once(flags[dev], configure);
         else configure();
     }
-    ad_particles<T, SMEM, BS, OM><<<grid, BS, smem, s>>>(L);
+    ad_particles<T, SMEM, BS, OM, UNIT><<<grid, BS, smem, s>>>(L);
 }
 
 template <class T, bool SMEM, int BS>
 void go(const AdLaunch& L, int64_t span, size_t smem, cudaStream_t s) {
     const int64_t nb = (span + BS - 1) / BS;
-    if (batched_obs_major(L, nb)) go_om<T, SMEM, BS, true>(L, nb, smem, s);
-    else go_om<T, SMEM, BS, false>(L, nb, smem, s);
+    if (L.unit_cpo > 0) go_om<T, SMEM, BS, false, true>(L, nb, smem, s);  // single-sample: grid order moot
+    else if (batched_obs_major(L, nb)) go_om<T, SMEM, BS, true, false>(L, nb, smem, s);
+    else go_om<T, SMEM, BS, false, false>(L, nb, smem, s);
 }
 
 template <class T>
