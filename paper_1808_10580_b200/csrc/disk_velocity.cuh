@@ -30,6 +30,12 @@ struct SmemCoef {
     template <int O>
     __device__ __forceinline__ void get2(T& a, T& b) const;
 };
+// The same block seen from a runtime offset of `off` elements (a row base in
+// the tiled disk kernel's row loop).
+template <class T>
+__device__ __forceinline__ SmemCoef<T> shifted(const SmemCoef<T>& C, int off) {
+    return SmemCoef<T>{C.base + static_cast<uint32_t>(off) * static_cast<uint32_t>(sizeof(T))};
+}
 template <>
 template <int O>
 __device__ __forceinline__ void SmemCoef<double>::get2(double& a, double& b) const {
@@ -92,6 +98,11 @@ struct ParamCoef {
         b = v.y;
     }
 };
+
+template <int K, class T>
+__device__ __forceinline__ ParamCoef<K, T> shifted(const ParamCoef<K, T>& C, int off) {  // off even
+    return ParamCoef<K, T>{C.P, C.zero + off / 2};
+}
 
 template <int O, int K>
 __device__ __forceinline__ void get4(const ParamCoef<K, float>& C, float& a, float& b, float& c, float& d) {
@@ -485,6 +496,68 @@ __device__ __forceinline__ void tiled_row0(const CA& C, const TilePowers<T>& W, 
     (tiled_row0_term<K, T0, Qs>(C, W, a0, a1), ...);
 }
 
+// Pair offsets of every row (4 doubles per pair) in the constant bank, for
+// the runtime row loop over a tile's full rows.
+template <int K>
+struct DiskRowOffsets {
+    int off[K + 2];
+    constexpr DiskRowOffsets() : off() {
+        for (int k1 = 1; k1 <= K + 1; ++k1) off[k1] = 4 * DiskShape<K>::pair_offset(k1);
+    }
+};
+template <int K>
+__constant__ DiskRowOffsets<K> c_disk_row_off = DiskRowOffsets<K>();
+
+template <int K, int T0>
+struct DiskTileFull {  // rows k1 = 1..full with all 8 pairs in this tile
+    static constexpr int full() {
+        int r = 0;
+        while (r < K && DiskTile<K, T0>::npair(r + 1) == kDiskTile) ++r;
+        return r;
+    }
+};
+
+template <int K, int T0, int K1, class T, class CA, int... K1s>
+__device__ __forceinline__ void tiled_rows_from(const CA& C, const TilePowers<T>& W, T c1, T s1, T& p1r, T& p1i,
+                                                T& acc1, T& acc2, std::integer_sequence<int, K1s...>) {
+    (tiled_row<K, T0, K1 + K1s>(C, W, c1, s1, p1r, p1i, acc1, acc2), ...);
+}
+
+// Hybrid tile (SMC_TILED_HYBRID): the full rows run through ONE 8-pair body
+// in a runtime loop (row base from the constant-bank offset table), only the
+// partial rows at the disk's edge are unrolled.  The fully unrolled form is
+// ~5800 instructions per step at K = 25 and stalls on instruction fetch (ncu:
+// no_instructions 44 % of samples).
+template <int K, int T0, class T, class CA>
+__device__ __forceinline__ void tiled_rows_hybrid(const CA& C, const TilePowers<T>& W, T c1, T s1, T& acc1,
+                                                  T& acc2) {
+    constexpr int F = DiskTileFull<K, T0>::full();
+    constexpr int R = DiskTile<K, T0>::rows();
+    T p1r = c1, p1i = s1;
+#pragma unroll 1
+    for (int k1 = 1; k1 <= F; ++k1) {
+        if (k1 > 1) {
+            const T nr = fma(p1r, c1, -p1i * s1);
+            p1i = fma(p1r, s1, p1i * c1);
+            p1r = nr;
+        }
+        T Ar = T(0), Ai = T(0), Br = T(0), Bi = T(0);
+        if constexpr (T0 == 0) shifted(C, DiskShape<K>::g0_offset + 2 * (k1 - 1)).template get2<0>(Ar, Ai);
+        // row k1's pairs j0+1..j0+8: the row-1 body (pair_offset(1) = 0) shifted to row k1
+        tiled_pairs<K, T0, 1>(shifted(C, c_disk_row_off<K>.off[k1]), W, Ar, Ai, Br, Bi,
+                              std::make_integer_sequence<int, kDiskTile>{});
+        const T kd = T(k1);
+        acc2 = fma(kd, fma(p1r, Ar, -p1i * Ai), acc2);
+        acc1 = fma(-p1r, Br, fma(p1i, Bi, acc1));
+    }
+    if constexpr (R > F)
+        tiled_rows_from<K, T0, F + 1>(C, W, c1, s1, p1r, p1i, acc1, acc2, std::make_integer_sequence<int, R - F>{});
+}
+
+#ifndef SMC_TILED_HYBRID
+#define SMC_TILED_HYBRID 1
+#endif
+
 template <int K, int T0, class T, class CA>
 __device__ __forceinline__ void tiled_tile(const CA& C, T c1, T s1, T c2, T s2, T& p2r, T& p2i, T& a0, T& a1,
                                            T& acc1, T& acc2) {
@@ -501,7 +574,8 @@ __device__ __forceinline__ void tiled_tile(const CA& C, T c1, T s1, T c2, T s2, 
         W.qi[q] = T(Tl::j0 + q + 1) * p2i;
     }
     tiled_row0<K, T0>(C, W, a0, a1, std::make_integer_sequence<int, Tl::w>{});
-    tiled_rows<K, T0>(C, W, c1, s1, acc1, acc2, std::make_integer_sequence<int, Tl::rows()>{});
+    if constexpr (SMC_TILED_HYBRID) tiled_rows_hybrid<K, T0>(C, W, c1, s1, acc1, acc2);
+    else tiled_rows<K, T0>(C, W, c1, s1, acc1, acc2, std::make_integer_sequence<int, Tl::rows()>{});
 }
 
 template <int K, class T, class CA, int... Ts>
