@@ -103,7 +103,8 @@ struct Forcing {
 // DISK_K > 0 (FP64, Fourier velocity filling the disk |k| <= DISK_K): the
 // compile-time disk series of K1 (disk_velocity.cuh) from a coefficient block
 // staged in shared memory, instead of the runtime-tiled lattice loop.
-template <class T, bool STRICT, int KCAP, int NB = 0, int VEL = 0, bool BASIS = false, int DISK_K = 0>
+// DOM: 1 = box domain compiled in (domain_contains<T, 1>), 0 = any kind.
+template <class T, bool STRICT, int KCAP, int NB = 0, int VEL = 0, bool BASIS = false, int DISK_K = 0, int DOM = 0>
 __global__ void __launch_bounds__(kBvpBlock) bvp_walkers(const BvpLaunch L) {
     constexpr unsigned FULL = 0xffffffffu;
     __shared__ __align__(16) T disk_coef[DISK_K > 0 ? DiskShape<DISK_K>::n_coef : 2];
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(kBvpBlock) bvp_walkers(const BvpLaunch L) {
             if constexpr (BASIS) forcing.basis(double(x1), double(x2), phi);
             else f = forcing(L.forcing, x1, x2);  // FP64, or the float variant for T = float
             ++my_steps;
-            if (!domain_contains<T>(L.domain, n1, n2)) {
+            if (!domain_contains<T, DOM>(L.domain, n1, n2)) {
                 T h1, h2;
                 const T frac = boundary_exit<T>(L.domain, x1, x2, n1, n2, h1, h2);
                 const T tau = T(double(step)) * dt + frac * dt;

@@ -9,21 +9,29 @@
 namespace smc {
 namespace {
 
-template <class T, int VEL>
+template <class T, int VEL, int DOM>
 void dispatch_nb(const BvpLaunch& L, int nb, unsigned blocks, cudaStream_t s) {
     switch (nb) {
-        case 1: bvp_walkers<T, false, 0, 1, VEL><<<blocks, kBvpBlock, 0, s>>>(L); break;
-        case 2: bvp_walkers<T, false, 0, 2, VEL><<<blocks, kBvpBlock, 0, s>>>(L); break;
-        case 3: bvp_walkers<T, false, 0, 3, VEL><<<blocks, kBvpBlock, 0, s>>>(L); break;
-        case 4: bvp_walkers<T, false, 0, 4, VEL><<<blocks, kBvpBlock, 0, s>>>(L); break;
-        default: bvp_walkers<T, false, 0, 0, VEL><<<blocks, kBvpBlock, 0, s>>>(L);
+        case 1: bvp_walkers<T, false, 0, 1, VEL, false, 0, DOM><<<blocks, kBvpBlock, 0, s>>>(L); break;
+        case 2: bvp_walkers<T, false, 0, 2, VEL, false, 0, DOM><<<blocks, kBvpBlock, 0, s>>>(L); break;
+        case 3: bvp_walkers<T, false, 0, 3, VEL, false, 0, DOM><<<blocks, kBvpBlock, 0, s>>>(L); break;
+        case 4: bvp_walkers<T, false, 0, 4, VEL, false, 0, DOM><<<blocks, kBvpBlock, 0, s>>>(L); break;
+        default: bvp_walkers<T, false, 0, 0, VEL, false, 0, DOM><<<blocks, kBvpBlock, 0, s>>>(L);
     }
+}
+
+// Box domains (the paper's Dirichlet problem, C3) get the box test compiled
+// in; other kinds keep the run-time selection.
+template <class T, int VEL>
+void dispatch_dom(const BvpLaunch& L, int nb, unsigned blocks, cudaStream_t s) {
+    if (L.domain.kind == 1) dispatch_nb<T, VEL, 1>(L, nb, blocks, s);
+    else dispatch_nb<T, VEL, 0>(L, nb, blocks, s);
 }
 
 template <class T>
 void dispatch(const BvpLaunch& L, int nb, unsigned blocks, cudaStream_t s) {
-    if (L.vel.is_constant) dispatch_nb<T, 1>(L, nb, blocks, s);
-    else dispatch_nb<T, 0>(L, nb, blocks, s);
+    if (L.vel.is_constant) dispatch_dom<T, 1>(L, nb, blocks, s);
+    else dispatch_dom<T, 0>(L, nb, blocks, s);
 }
 
 // Persistent blocks per SM (tuning knob SMC_BVP_BPS; 8, 12 and 16 measured

@@ -14,8 +14,11 @@ struct DomainImg {
     double c1, c2, r, r2;       // disk (r2 = r * r)
 };
 
-template <class T>
+// KIND: 0 = the kind read at run time; 1 (box) / 2 (disk) compile the test
+// for that kind only (the walker kernels' box instantiation).
+template <class T, int KIND = 0>
 __device__ __forceinline__ bool domain_contains(const DomainImg& d, T x1, T x2) {
+    if constexpr (KIND == 1) return (x1 > T(d.lo1)) & (x1 < T(d.hi1)) & (x2 > T(d.lo2)) & (x2 < T(d.hi2));
     // both tests evaluated, then selected: no branch on the (uniform) kind in
     // the walker loop, so the step stays one basic block
     const bool in_box = (x1 > T(d.lo1)) & (x1 < T(d.hi1)) & (x2 > T(d.lo2)) & (x2 < T(d.hi2));
