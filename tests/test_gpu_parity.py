@@ -355,7 +355,7 @@ def test_fp32_param_path_matches_shared_memory_path(ctx, golden, monkeypatch):
         assert np.array_equal(x, y), float(np.max(np.abs(x - y)))
 
 
-@pytest.mark.parametrize("K", [1, 5, 12])
+@pytest.mark.parametrize("K", [1, 5, 12, 25])
 def test_fp32_param_path_matches_batched_path(ctx, K):
     """The packed FP32 kernel-parameter form (FFMA2) against the batched
     shared-memory kernel on the same single sample, across the disk sizes:
@@ -371,13 +371,14 @@ def test_fp32_param_path_matches_batched_path(ctx, K):
         assert batched[0, j]["mean"] == e.mean and batched[0, j]["std_error"] == e.std_error, j
 
 
-@pytest.mark.parametrize("disable_disk", [False, True])
-def test_fp32_tiled_kernel_within_three_standard_errors(ctx, monkeypatch, disable_disk):
-    """The FP32 tiled lattice kernel (packed FFMA2 pair updates, K > 12 or
-    SMC_DISABLE_DISK) against the FP64 parity path on the same streams."""
+@pytest.mark.parametrize("disable_disk,K", [(False, 14), (False, 25), (True, 6)])
+def test_fp32_tiled_kernel_within_three_standard_errors(ctx, monkeypatch, disable_disk, K):
+    """The FP32 tiled kernels (packed FFMA2 pair updates: the generic lattice
+    at K = 14 or under SMC_DISABLE_DISK, the tiled disk at K = 25) against
+    the FP64 parity path on the same streams."""
     if disable_disk:
         monkeypatch.setenv("SMC_DISABLE_DISK", "1")
-    prior = S.PriorSpec(14 if not disable_disk else 6, 1.0, 2.5)
+    prior = S.PriorSpec(K, 1.0, 2.5)
     U = np.random.default_rng(3).normal(size=(2, prior.dimension())) * 0.5
     b64 = S.observe_ad_batched(specs.c4_base(n_particles=4000), prior, U, 12, ctx=ctx)
     b32 = S.observe_ad_batched(specs.c4_base(n_particles=4000, precision=S.Precision.fp32), prior, U, 12, ctx=ctx)
@@ -581,3 +582,33 @@ def test_concurrent_contexts_do_not_interfere():
     assert out[0] == serial[0] and out[1] == serial[1] and out[2] == serial_b
     for c in ctxs:
         c.close()
+
+
+def test_k25_dense_field_paths(ctx, port, monkeypatch):
+    """The tiled disk kernels (K = 25, the C4 prior): the single-sample
+    shared-memory form, the batched form and the unit-mode parameter form
+    (a 3-rank group on one GPU) give identical estimates; the runtime-tiled
+    lattice kernel agrees to rounding; particles are the oracle's."""
+    prior = specs.C4_PRIOR
+    u = S.prior_draw(prior, 808, 0xBE9C4, 1, ctx)
+    spec = specs.c4_base(n_particles=1500)
+    spec.velocity = S.VelocityField.fourier(S.velocity_from_coefficients(prior, u))
+    disk = S.observe_ad(spec, 808, ctx=ctx)
+    batched = S.observe_ad_batched(specs.c4_base(n_particles=1500), prior, u[None, :], 808, ctx=ctx)
+    grouped = S.observe_ad(spec, 808, ctx=S.Context(devices=[0, 0, 0]))
+    for j, e in enumerate(disk):
+        assert (batched[0, j]["mean"], batched[0, j]["std_error"]) == (e.mean, e.std_error)
+        assert (grouped[j].mean, grouped[j].std_error) == (e.mean, e.std_error)
+    for j in (0, 4, 8):
+        vals = S.ad_particle_values(spec, j, 808, 64, ctx)
+        assert np.max(np.abs(vals - port.ad_particle_values(spec, j, 808, 64))) < 1e-11
+    spec32 = specs.c4_base(n_particles=1500, precision=S.Precision.fp32)
+    spec32.velocity = spec.velocity
+    single32 = S.observe_ad(spec32, 808, ctx=ctx)
+    grouped32 = S.observe_ad(spec32, 808, ctx=S.Context(devices=[0, 0]))
+    assert [(e.mean, e.std_error) for e in single32] == [(e.mean, e.std_error) for e in grouped32]
+    assert all(abs(a.mean - b.mean) <= 3.0 * b.std_error for a, b in zip(single32, disk))
+    monkeypatch.setenv("SMC_DISABLE_DISK", "1")
+    lattice = S.observe_ad(spec, 808, ctx=ctx)
+    for a, b in zip(lattice, disk):
+        assert abs(a.mean - b.mean) <= 1e-12 and abs(a.std_error - b.std_error) <= 1e-10 * b.std_error
