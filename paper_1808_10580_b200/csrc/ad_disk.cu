@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(kBlock, MINB)
     auto vel = [&](const T (&x1)[1], const T (&x2)[1], T (&v1)[1], T (&v2)[1], int zero) {
                              if constexpr (std::is_same<T, float>::value) {
                                  const PackedCoef<K> C{P};
-                                 velocity_disk_any<K, T>(C, x1, x2, v1, v2);
+                                 velocity_disk<K, T, 1>(C, x1, x2, v1, v2);
                              } else {
                                  const ParamCoef<K, T> C{P, zero};
                                  velocity_disk_any<K, T>(C, x1, x2, v1, v2);
@@ -204,8 +204,11 @@ cudaError_t dispatch_param(const AdLaunch& L, int K, cudaStream_t s) {
         case 10: return launch_param<10, T>(L, s);
         case 11: return launch_param<11, T>(L, s);
         case 12: return launch_param<12, T>(L, s);
-        case 25: return launch_param<25, T>(L, s);  // unit mode only (launch_ad_disk)
-        default: return cudaErrorNotSupported;
+        default:
+            if constexpr (std::is_same<T, double>::value) {
+                if (K == 25) return launch_param<25, T>(L, s);
+            }
+            return cudaErrorNotSupported;
     }
 }
 
@@ -255,7 +258,7 @@ cudaError_t dispatch_p(const AdLaunch& L, int K, const double* c, cudaStream_t s
         case 11: return launch_k<11, T, P, MinBlocks<11, P>::value>(L, c, s);
         case 12: return launch_k<12, T, P, MinBlocks<12, P>::value>(L, c, s);
         default:
-            if constexpr (P == 1) {
+            if constexpr (std::is_same<T, double>::value && P == 1) {
                 if (K == 25) return launch_k<25, T, 1, MinBlocks<25, 1>::value>(L, c, s);
             }
             return cudaErrorNotSupported;

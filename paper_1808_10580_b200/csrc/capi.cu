@@ -226,7 +226,7 @@ AdImage build_ad_image(const smc_ad_problem& p, const std::vector<const Prepared
     // Dense fields with a compile-time disk kernel for their K take it
     // (K <= kDiskMaxK; FP64 also the tiled disk kernels' K).
     const bool disk = !structure.is_constant && p.precision != SMC_FP64_STRICT &&
-                      disk_kernel_for(structure.K) &&
+                      disk_kernel_for(structure.K, p.precision == SMC_FP64) &&
                       2 * structure.modes.size() >= static_cast<size_t>(disk_n_modes(structure.K)) &&
                       std::getenv("SMC_DISABLE_DISK") == nullptr;
     if (disk) {

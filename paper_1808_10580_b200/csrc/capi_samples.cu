@@ -251,7 +251,7 @@ void pcn_chains_impl(smc_ctx* ctx, const smc_ad_problem* forward, const smc_prio
     // (disk layout for K <= kDiskMaxK, tiled lattice otherwise)
     const PreparedVelocity structure = prior_structure(prior->cutoff);
     const bool use_disk =
-        disk_kernel_for(prior->cutoff) && std::getenv("SMC_DISABLE_DISK") == nullptr;
+        disk_kernel_for(prior->cutoff, p.precision == SMC_FP64) && std::getenv("SMC_DISABLE_DISK") == nullptr;
     const LatticeHost Lh = lattice_structure(structure);
     const PackMap pmap = pack_map(prior->cutoff, use_disk, &Lh);
     const int64_t stride = pmap.stride;

@@ -36,11 +36,11 @@ struct DiskShape {
 
 // Largest K with the register-resident disk kernel.
 constexpr int kDiskMaxK = 12;
-// Tiled compile-time disk kernels (disk_velocity.cuh velocity_disk_tiled;
-// K1, FP64 and the packed FP32 form) exist for these K above kDiskMaxK.
+// Tiled compile-time disk kernels (disk_velocity.cuh velocity_disk_tiled,
+// FP64 K1 only) exist for these K above kDiskMaxK.
 inline bool disk_tiled_instantiated(int K) { return K == 25; }
 // Whether K1 has a compile-time disk kernel for a dense field of cutoff K.
-inline bool disk_kernel_for(int K) { return K <= kDiskMaxK || disk_tiled_instantiated(K); }
+inline bool disk_kernel_for(int K, bool fp64) { return K <= kDiskMaxK || (fp64 && disk_tiled_instantiated(K)); }
 
 inline int disk_jmax(int K, int k1) {
     int j = 0;

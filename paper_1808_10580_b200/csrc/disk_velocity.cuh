@@ -136,7 +136,6 @@ struct alignas(16) PackedParam {
 template <int K>
 struct PackedCoef {
     const PackedParam<K>& P;
-    int pair0 = 0;  // pair shift (the tiled disk kernel's run-time row base; 0 otherwise)
     template <int O>  // O: offset in the disk_shape.h layout (row0 / g0 only)
     __device__ __forceinline__ void get2(float& a, float& b) const {
         static_assert(O >= DiskShape<K>::row0_offset, "pairs use pair4");
@@ -145,7 +144,7 @@ struct PackedCoef {
     }
     template <int I>  // the I-th pair's four coefficient pairs
     __device__ __forceinline__ void pair4(uint64_t& c0, uint64_t& c1, uint64_t& c2, uint64_t& c3) const {
-        const ulonglong2* q = reinterpret_cast<const ulonglong2*>(P.c) + 2 * (pair0 + I);
+        const ulonglong2* q = reinterpret_cast<const ulonglong2*>(P.c) + 2 * I;
         const ulonglong2 u = q[0], v = q[1];
         c0 = u.x;
         c1 = u.y;
@@ -172,31 +171,6 @@ struct PackedSmemCoef {
 };
 // Stage one sample's packed FP32 block (PackedShape layout) from its
 // disk_shape.h double block; all threads of the block cooperate.
-// Pair-granular shift (off in the disk_shape.h double layout, 4 per pair)
-// and a run-time-offset load of a row0 / g0 coefficient pair.
-template <int K>
-__device__ __forceinline__ PackedSmemCoef<K> shifted(const PackedSmemCoef<K>& C, int off) {
-    return PackedSmemCoef<K>{C.base + static_cast<uint32_t>(off) * 8u};
-}
-template <int K>
-__device__ __forceinline__ void get2_at(const PackedSmemCoef<K>& C, int O, float& a, float& b) {
-    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];"
-                 : "=f"(a), "=f"(b)
-                 : "r"(C.base + static_cast<uint32_t>(O + PackedShape<K>::shift) * 4u));
-}
-template <int K>
-__device__ __forceinline__ PackedCoef<K> shifted(const PackedCoef<K>& C, int off) {
-    return PackedCoef<K>{C.P, C.pair0 + off / 4};
-}
-template <int K>
-__device__ __forceinline__ void get2_at(const PackedCoef<K>& C, int O, float& a, float& b) {
-    a = C.P.c[O + PackedShape<K>::shift];
-    b = C.P.c[O + PackedShape<K>::shift + 1];
-}
-template <class CA, class T>
-__device__ __forceinline__ void get2_at(const CA& C, int O, T& a, T& b) {
-    shifted(C, O).template get2<0>(a, b);
-}
 template <int K>
 __device__ __forceinline__ void stage_packed(float* dst, const double* src, int tid, int nthreads) {
     for (int i = tid; i < DiskShape<K>::n_pairs; i += nthreads) {
@@ -480,29 +454,10 @@ __device__ __forceinline__ void tiled_pair(const CA& C, const TilePowers<T>& W, 
     Bi = fma(ar, W.qi[Q], Bi);
 }
 
-// FP32 packed block (PackedSmemCoef): four FFMA2 per pair on the expanded
-// coefficient pairs, as disk_pair_packed.
-template <int K, int T0, int K1, int Q, class CA, class W_t>
-__device__ __forceinline__ void tiled_pair_packed(const CA& C, const W_t& W, uint64_t& A, uint64_t& B) {
-    uint64_t c0, c1, c2, c3;
-    C.template pair4<DiskShape<K>::pair_offset(K1) + DiskTile<K, T0>::j0 + Q>(c0, c1, c2, c3);
-    f2_fma_bcast(A, c0, W.pr[Q]);
-    f2_fma_bcast(B, c1, W.qr[Q]);
-    f2_fma_bcast(A, c2, W.pi[Q]);
-    f2_fma_bcast(B, c3, W.qi[Q]);
-}
-
 template <int K, int T0, int K1, class T, class CA, int... Qs>
 __device__ __forceinline__ void tiled_pairs(const CA& C, const TilePowers<T>& W, T& Ar, T& Ai, T& Br, T& Bi,
                                             std::integer_sequence<int, Qs...>) {
-    if constexpr (IsPacked<CA>::value) {
-        uint64_t A = f2_pack(Ar, Ai), B = f2_pack(Br, Bi);
-        (tiled_pair_packed<K, T0, K1, Qs>(C, W, A, B), ...);
-        f2_unpack(A, Ar, Ai);
-        f2_unpack(B, Br, Bi);
-    } else {
-        (tiled_pair<K, T0, K1, Qs>(C, W, Ar, Ai, Br, Bi), ...);
-    }
+    (tiled_pair<K, T0, K1, Qs>(C, W, Ar, Ai, Br, Bi), ...);
 }
 
 template <int K, int T0, int K1, class T, class CA>
@@ -587,7 +542,7 @@ __device__ __forceinline__ void tiled_rows_hybrid(const CA& C, const TilePowers<
             p1r = nr;
         }
         T Ar = T(0), Ai = T(0), Br = T(0), Bi = T(0);
-        if constexpr (T0 == 0) get2_at(C, DiskShape<K>::g0_offset + 2 * (k1 - 1), Ar, Ai);
+        if constexpr (T0 == 0) shifted(C, DiskShape<K>::g0_offset + 2 * (k1 - 1)).template get2<0>(Ar, Ai);
         // row k1's pairs j0+1..j0+8: the row-1 body (pair_offset(1) = 0) shifted to row k1
         tiled_pairs<K, T0, 1>(shifted(C, c_disk_row_off<K>.off[k1]), W, Ar, Ai, Br, Bi,
                               std::make_integer_sequence<int, kDiskTile>{});

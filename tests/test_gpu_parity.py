@@ -373,9 +373,9 @@ def test_fp32_param_path_matches_batched_path(ctx, K):
 
 @pytest.mark.parametrize("disable_disk,K", [(False, 14), (False, 25), (True, 6)])
 def test_fp32_tiled_kernel_within_three_standard_errors(ctx, monkeypatch, disable_disk, K):
-    """The FP32 tiled kernels (packed FFMA2 pair updates: the generic lattice
-    at K = 14 or under SMC_DISABLE_DISK, the tiled disk at K = 25) against
-    the FP64 parity path on the same streams."""
+    """The FP32 tiled lattice kernel (packed FFMA2 pair updates; FP32 dense
+    fields above K = 12 take it too — the tiled disk kernel is FP64 only)
+    against the FP64 parity path on the same streams."""
     if disable_disk:
         monkeypatch.setenv("SMC_DISABLE_DISK", "1")
     prior = S.PriorSpec(K, 1.0, 2.5)
