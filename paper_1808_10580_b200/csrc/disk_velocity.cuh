@@ -404,15 +404,16 @@ __device__ __forceinline__ void velocity_disk(const CA& C, const T (&x1)[P], con
 // Tiled disk series for kDiskMaxK < K (FP64 K1; disk_tiled_instantiated():
 // the batched C4 prior has K = 25, M = 980).  Powers for every j no longer
 // fit in registers, so the columns run in tiles of 8 (P2[j], Q[j] of one tile
-// in registers, continued by complex products from the previous tile), and
-// inside a tile every row k1 with modes there unrolls exactly its pairs —
-// the shape is known at compile time, so unlike the generic tiled kernel
-// (velocity.cuh) no pair slot is padding, no coefficient address is
-// computed at run time and the loop has no trip counts.  Same disk_shape.h
-// coefficient layout as the K <= 12 kernel.  Per (tile, row): P1 <- P1 e1
-// (restarted each tile) and the fold v2 += k1 Re(P1 A), v1 -= Re(P1 B').
-// Measured and rejected: interleaving the pair updates of two rows (eight
-// accumulator chains instead of four): C4 2974 -> 3032 ms.
+// in registers, continued by complex products from the previous tile).  The
+// shape is known at compile time: a tile's full rows (8 pairs) share one
+// body in a run-time row loop, the partial rows at the disk's edge are
+// unrolled with exactly their pairs, so unlike the generic tiled kernel
+// (velocity.cuh) no pair slot is padding.  Same disk_shape.h coefficient
+// layout as the K <= 12 kernel.  Per (tile, row): P1 <- P1 e1 (restarted
+// each tile) and the fold v2 += k1 Re(P1 A), v1 -= Re(P1 B').  Measured and
+// rejected: unrolling every row (instruction-fetch bound, C4 2969 vs 2763
+// ms) and interleaving the pair updates of two rows (eight accumulator
+// chains instead of four: 2974 -> 3032 ms).
 constexpr int kDiskTile = 8;
 
 template <int K, int T0>
@@ -475,13 +476,6 @@ __device__ __forceinline__ void tiled_row(const CA& C, const TilePowers<T>& W, T
     acc1 = fma(-p1r, Br, fma(p1i, Bi, acc1));
 }
 
-template <int K, int T0, class T, class CA, int... K1s>
-__device__ __forceinline__ void tiled_rows(const CA& C, const TilePowers<T>& W, T c1, T s1, T& acc1, T& acc2,
-                                           std::integer_sequence<int, K1s...>) {
-    T p1r = c1, p1i = s1;
-    (tiled_row<K, T0, K1s + 1>(C, W, c1, s1, p1r, p1i, acc1, acc2), ...);
-}
-
 template <int K, int T0, int Q, class T, class CA>
 __device__ __forceinline__ void tiled_row0_term(const CA& C, const TilePowers<T>& W, T& a0, T& a1) {
     T gr, gi;
@@ -523,7 +517,7 @@ __device__ __forceinline__ void tiled_rows_from(const CA& C, const TilePowers<T>
     (tiled_row<K, T0, K1 + K1s>(C, W, c1, s1, p1r, p1i, acc1, acc2), ...);
 }
 
-// Hybrid tile (SMC_TILED_HYBRID): the full rows run through ONE 8-pair body
+// Rows of a tile: the full rows run through ONE 8-pair body
 // in a runtime loop (row base from the constant-bank offset table), only the
 // partial rows at the disk's edge are unrolled.  The fully unrolled form is
 // ~5800 instructions per step at K = 25 and stalls on instruction fetch (ncu:
@@ -554,10 +548,6 @@ __device__ __forceinline__ void tiled_rows_hybrid(const CA& C, const TilePowers<
         tiled_rows_from<K, T0, F + 1>(C, W, c1, s1, p1r, p1i, acc1, acc2, std::make_integer_sequence<int, R - F>{});
 }
 
-#ifndef SMC_TILED_HYBRID
-#define SMC_TILED_HYBRID 1
-#endif
-
 template <int K, int T0, class T, class CA>
 __device__ __forceinline__ void tiled_tile(const CA& C, T c1, T s1, T c2, T s2, T& p2r, T& p2i, T& a0, T& a1,
                                            T& acc1, T& acc2) {
@@ -574,8 +564,7 @@ __device__ __forceinline__ void tiled_tile(const CA& C, T c1, T s1, T c2, T s2, 
         W.qi[q] = T(Tl::j0 + q + 1) * p2i;
     }
     tiled_row0<K, T0>(C, W, a0, a1, std::make_integer_sequence<int, Tl::w>{});
-    if constexpr (SMC_TILED_HYBRID) tiled_rows_hybrid<K, T0>(C, W, c1, s1, acc1, acc2);
-    else tiled_rows<K, T0>(C, W, c1, s1, acc1, acc2, std::make_integer_sequence<int, Tl::rows()>{});
+    tiled_rows_hybrid<K, T0>(C, W, c1, s1, acc1, acc2);
 }
 
 template <int K, class T, class CA, int... Ts>
