@@ -156,14 +156,14 @@ def test_batched_equals_single_calls(ctx):
             assert abs(out[b, j]["std_error"] - e.std_error) <= 1e-12 * e.std_error
 
 
-@pytest.mark.parametrize("K,n_particles", [(8, 160), (8, 100), (3, 40), (14, 96)])
+@pytest.mark.parametrize("K,n_particles", [(8, 160), (8, 100), (3, 40), (14, 96), (25, 160), (25, 70)])
 def test_batched_grid_orders_identical(ctx, monkeypatch, K, n_particles):
     """Batched launches pick a grid order (sample-major; observation-major
     longest-first; observation-major over flattened (sample, particle)
     ranges) by launch size.  Every particle's path is addressed by (seed, obs,
     particle, step), so all orders give bit-identical estimates — including
-    particle counts that are not a multiple of 32 (warps straddle samples) and
-    the generic tiled kernel (K > 12)."""
+    particle counts that are not a multiple of 32 (warps straddle samples), the
+    generic tiled kernel (K = 14) and the tiled disk kernel (K = 25)."""
     prior = S.PriorSpec(K, 1.0, 2.5)
     U = np.random.default_rng(K).normal(size=(7, prior.dimension())) * 0.3
     base = specs.c4_base(n_particles=n_particles)

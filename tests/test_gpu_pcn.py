@@ -75,3 +75,17 @@ def test_graph_replay_matches_step_loop(ctx, monkeypatch, n_steps, burn_in, thin
     graph = S.run_chains(cfg, prior, likelihood(), seeds, ctx=ctx)
     for key in ("phi_trace", "final_u", "map_u", "map_objective", "accepted", "samples"):
         assert np.array_equal(np.asarray(loop[key]), np.asarray(graph[key])), key
+
+
+def test_k25_chains_match_reference(ctx, reference):
+    """Chains on the C4 prior (K = 25, dimension 1960): the device pCN driver
+    then runs the tiled disk kernel every step; two short chains against the
+    reference's run_chain (workers = all host cores)."""
+    prior = S.PriorSpec(25, 1.0, 2.5)
+    cfg = S.ChainConfig(n_steps=6, beta=0.05, burn_in=1, thin=2)
+    res = S.run_chains(cfg, prior, likelihood(), [21, 22], ctx=ctx)
+    for b, seed in enumerate((21, 22)):
+        ref = reference.run_chain(likelihood(), prior, 6, 0.05, 1, 2, seed)
+        assert res["accepted"][b] == ref["accepted"]
+        assert np.allclose(res["phi_trace"][b], ref["phi_trace"], rtol=1e-8, atol=1e-10)
+        assert np.allclose(res["final_u"][b], ref["final_u"], rtol=0, atol=1e-12)
