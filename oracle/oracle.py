@@ -236,7 +236,8 @@ class Reference(_Checker):
         `like` (paper_1808_10580_b200.LikelihoodSpec)."""
         p, keep = like.forward._pod() if like is not None else (None, None)
         dim = prior.dimension()
-        n_samples = max(0, (n_steps - max(burn_in, 0) - 1) // thin + 1) if n_steps > burn_in else 0
+        # the reference's sample iterations (inference.cpp:183-185)
+        n_samples = sum(1 for i in range(1, n_steps + 1) if i > burn_in and (i - burn_in - 1) % thin == 0)
         trace = np.zeros(max(n_steps, 1))
         samples = np.zeros((max(n_samples, 1), dim))
         final_u = np.zeros(dim)

@@ -58,26 +58,34 @@ __device__ __forceinline__ void with_smem_coef(const T* staged, Body&& body) {
     else body(SmemCoef<T>{base});
 }
 
-template <int K, class T, int P, int MINB>
+// UNIT: unit mode (a sharded single-sample launch, kernels.h; P = 1, grid
+// y = 1) — the tiled disk kernels' form for group contexts (their parameter
+// form reads its coefficients by run-time row offsets: 87.8 vs 72.2 ms).
+template <int K, class T, int P, int MINB, bool UNIT = false>
 __global__ void __launch_bounds__(kBlock, MINB) ad_particles_disk(const AdLaunch L, const double* coef) {
     // this sample's coefficient block -> shared memory (compute type)
     __shared__ __align__(16) T staged[kStagedFloats<K, T, P>];
-    const int sample = L.obs_major ? blockIdx.y : blockIdx.z;
+    const int sample = UNIT ? 0 : (L.obs_major ? blockIdx.y : blockIdx.z);
     stage_sample<K, T, P>(staged, coef + static_cast<int64_t>(sample) * DiskShape<K>::n_coef);
     __syncthreads();
-    const int obs = __ldg(L.obs_order + (L.obs_major ? blockIdx.z : blockIdx.y));
-    const int64_t span = L.p_end - L.p_begin;
+    int obs = UNIT ? 0 : __ldg(L.obs_order + (L.obs_major ? blockIdx.z : blockIdx.y));
+    int64_t span = L.p_end - L.p_begin;
     const int64_t base = static_cast<int64_t>(blockIdx.x) * kBlock * P + threadIdx.x;
     if (base >= span) return;
     int64_t local[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) local[p] = base + static_cast<int64_t>(p) * kBlock;
+    if constexpr (UNIT) {
+        static_assert(P == 1, "unit mode: one particle per thread");
+        if (!unit_coords(L, base, obs, local[0])) return;
+        span = L.n_particles;
+    }
     with_smem_coef<K, T, P>(staged, [&](const auto& C) {
         auto vel = [&](const T (&x1)[P], const T (&x2)[P], T (&v1)[P], T (&v2)[P], int) {
             if constexpr (P == 1) velocity_disk_any<K, T>(C, x1, x2, v1, v2);
             else velocity_disk<K, T, P>(C, x1, x2, v1, v2);
         };
-        ad_particles_p<T, P, decltype(vel)&, false, false>(L, obs, sample, local, span, vel);  // never unit mode
+        ad_particles_p<T, P, decltype(vel)&, false, UNIT>(L, obs, sample, local, span, vel);
     });
 }
 
@@ -217,6 +225,12 @@ cudaError_t launch_k(const AdLaunch& L, const double* coef, cudaStream_t s) {
     const int64_t span = L.p_end - L.p_begin;
     const int64_t per_block = static_cast<int64_t>(kBlock) * P;
     const int64_t nb = (span + per_block - 1) / per_block;
+    if constexpr (P == 1 && K > kDiskMaxK) {
+        if (L.unit_cpo > 0) {
+            ad_particles_disk<K, T, 1, MINB, true><<<dim3(static_cast<unsigned>(nb), 1, 1), kBlock, 0, s>>>(L, coef);
+            return cudaGetLastError();
+        }
+    }
     AdLaunch LB = L;
     LB.obs_major = batched_obs_major(L, nb);
     if constexpr (P == 1) {
@@ -285,11 +299,12 @@ cudaError_t launch_ad_disk(const AdLaunch& L, int K, const double* coef, cudaStr
     // one coefficient block with its host copy: the kernel-parameter path
     // (SMC_DISK_P=2 keeps the shared-memory kernel, which has the P=2 form)
     const char* pe = std::getenv("SMC_DISK_P");
-    // The tiled disk kernels (K > kDiskMaxK) take the parameter path only in
-    // unit mode: their parameter form spills (K = 25 single sample: 80.6 ms
-    // vs 77.0 ms staged in shared memory).
+    // The tiled disk kernels (K > kDiskMaxK) stay in shared memory, in unit
+    // mode too: their parameter form reads run-time row offsets (K = 25
+    // single sample: 87.8 vs 72.2 ms; SMC_DISK_PARAM=1 selects it for A/B).
     if (L.n_samples == 1 && L.host_disk && !L.seeds &&
-        (L.unit_cpo > 0 || (K <= kDiskMaxK && !(pe && std::atoi(pe) == 2))))
+        (K <= kDiskMaxK || std::getenv("SMC_DISK_PARAM") != nullptr) &&
+        (L.unit_cpo > 0 || K > kDiskMaxK || !(pe && std::atoi(pe) == 2)))
         return L.precision == 1 ? dispatch_param<float>(L, K, s) : dispatch_param<double>(L, K, s);
     return L.precision == 1 ? dispatch<float>(L, K, coef, s) : dispatch<double>(L, K, coef, s);
 }

@@ -191,10 +191,15 @@ smc_status smc_ad_observe_batched(smc_ctx* ctx, const smc_ad_problem* base, cons
 }
 
 int64_t smc_pcn_num_samples(const smc_chain_config* cfg) {
-    // iterations i = 1..n_steps with i > burn_in and (i - burn_in - 1) % thin == 0
-    if (!cfg || cfg->thin < 1 || cfg->n_steps <= cfg->burn_in) return 0;
-    const int64_t burn = cfg->burn_in < 0 ? 0 : cfg->burn_in;
-    return (cfg->n_steps - burn - 1) / cfg->thin + 1;
+    // iterations i = 1..n_steps with i > burn_in and (i - burn_in - 1) % thin
+    // == 0 (inference.cpp:183-185): from the first such i0 every thin-th one.
+    // A negative burn_in moves i0 off 1 (burn_in = -2, thin 4: i0 = 3).
+    if (!cfg || cfg->thin < 1 || cfg->n_steps < 1) return 0;
+    const int64_t thin = cfg->thin;
+    const int64_t lo = cfg->burn_in + 1 > 1 ? cfg->burn_in + 1 : 1;
+    const int64_t r = ((lo - cfg->burn_in - 1) % thin + thin) % thin;
+    const int64_t i0 = r == 0 ? lo : lo + (thin - r);
+    return cfg->n_steps >= i0 ? (cfg->n_steps - i0) / thin + 1 : 0;
 }
 
 }  // extern "C"

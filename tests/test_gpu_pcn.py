@@ -89,3 +89,18 @@ def test_k25_chains_match_reference(ctx, reference):
         assert res["accepted"][b] == ref["accepted"]
         assert np.allclose(res["phi_trace"][b], ref["phi_trace"], rtol=1e-8, atol=1e-10)
         assert np.allclose(res["final_u"][b], ref["final_u"], rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("burn_in,thin", [(-2, 4), (-5, 3), (3, 5)])
+def test_sample_schedule_matches_reference(ctx, reference, burn_in, thin):
+    """The recorded iterations (i > burn_in, (i - burn_in - 1) % thin == 0,
+    inference.cpp:183-185), negative burn-in included: same sample count and
+    states as the reference's run_chain."""
+    prior = S.PriorSpec(2, 0.6, 2.5)
+    n = 17
+    res = S.run_chains(S.ChainConfig(n_steps=n, beta=0.3, burn_in=burn_in, thin=thin), prior, likelihood(), [9],
+                       ctx=ctx)
+    ref = reference.run_chain(likelihood(), prior, n, 0.3, burn_in, thin, 9)
+    want = [i for i in range(1, n + 1) if i > burn_in and (i - burn_in - 1) % thin == 0]
+    assert res["samples"].shape[1] == len(want) == ref["samples"].shape[0]
+    assert np.allclose(res["samples"][0], ref["samples"], rtol=0, atol=1e-12)
