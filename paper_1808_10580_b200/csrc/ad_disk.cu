@@ -193,7 +193,13 @@ cudaError_t launch_param(const AdLaunch& L, cudaStream_t s) {
                     static_cast<unsigned>(L.unit_cpo > 0 ? 1 : L.n_obs), 1);
     AdLaunch LK = L;
     LK.rk = make_round_keys(L.seed);
-    ad_particles_disk_param<K, T, (K <= 8 ? 4 : (K <= kDiskMaxK ? 3 : SMC_TILED_MINB))><<<grid, kBlock, 0, s>>>(LK, P);
+    // resident blocks per SM: FP64 with 5 <= K <= 8 runs 5 (96 registers; C2
+    // 31.9 -> 31.5 ms; 6 blocks at 80 registers spill: 32.3 ms); 4 below (C1
+    // is a small latency-bound launch: 0.34 ms at 4, 0.36 at 5) and for FP32
+    // (the packed block spills 300 B at 96 registers)
+    constexpr bool kFive = std::is_same<T, double>::value && K >= 5 && K <= 8;
+    constexpr int kMinB = kFive ? 5 : (K <= 8 ? 4 : (K <= kDiskMaxK ? 3 : SMC_TILED_MINB));
+    ad_particles_disk_param<K, T, kMinB><<<grid, kBlock, 0, s>>>(LK, P);
     return cudaGetLastError();
 }
 
