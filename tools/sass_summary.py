@@ -17,7 +17,7 @@ OBJ = ROOT / "paper_1808_10580_b200" / "lib" / "obj"
 
 # (label, object, mangled-name regex)
 KERNELS = [
-    ("K1 disk, parameter coefficients, K=8 FP64 (C2)", "ad_disk", r"ad_particles_disk_paramILi8EdLi4E"),
+    ("K1 disk, parameter coefficients, K=8 FP64 (C2)", "ad_disk", r"ad_particles_disk_paramILi8EdLi5E"),
     ("K1 tiled disk, shared memory, K=25 FP64 batched (C4)", "ad_disk", r"17ad_particles_diskILi25EdLi1ELi4E"),
     ("K1 generic tiled lattice, 512 threads FP64 (C5)", "ad_kernels", r"ad_particlesIdLb1ELi512ELb0ELb0E"),
     ("K1 disk, packed FFMA2, K=8 FP32 (C2 FP32)", "ad_disk", r"ad_particles_disk_paramILi8EfLi4E"),
