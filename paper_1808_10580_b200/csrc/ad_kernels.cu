@@ -22,12 +22,16 @@ constexpr size_t kSmemLimit = 64 * 1024;   // tables up to here: 256-thread bloc
 constexpr size_t kSmemMax = 220 * 1024;    // larger tables: one 512-thread block per SM
 constexpr size_t kSmemHard = 227 * 1024;
 constexpr int kMaxDevices = 64;
+// threads of the one-block-per-SM path for large staged tables (C5)
+#ifndef SMC_BIG_BLOCK
+#define SMC_BIG_BLOCK 512
+#endif
 
 // UNIT: the launch is in unit mode (sharded single-sample launches,
 // kernels.h); a compile-time flag so the unsharded kernel carries none of it
 // (as a runtime branch it cost C5 7 %: 4634 -> 4966 ms).
 template <class T, bool SMEM, int kBlock, bool OM, bool UNIT>
-__global__ void __launch_bounds__(kBlock, 512 / kBlock) ad_particles(const AdLaunch L) {
+__global__ void __launch_bounds__(kBlock, (512 / kBlock > 0 ? 512 / kBlock : 1)) ad_particles(const AdLaunch L) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // OM: grid (particle blocks, samples, observations longest first);
     // otherwise (particle blocks, observations, samples)
@@ -100,7 +104,7 @@ cudaError_t launch(const AdLaunch& L, cudaStream_t s) {
     const size_t smem = L.vel.is_constant ? 0 : static_cast<size_t>(L.vel.lat.sample_stride) * sizeof(T);
     if (std::getenv("SMC_LATTICE_GLOBAL") != nullptr || smem > kSmemMax) go<T, false, 256>(L, span, 0, s);
     else if (smem <= kSmemLimit) go<T, true, 256>(L, span, smem, s);
-    else go<T, true, 512>(L, span, smem, s);
+    else go<T, true, SMC_BIG_BLOCK>(L, span, smem, s);
     return cudaGetLastError();
 }
 

@@ -27,6 +27,15 @@
 namespace smc {
 
 constexpr int kBvpBlock = 128;
+// Minimum resident walker blocks per SM the register allocation must allow,
+// for the constant-velocity walkers (the paper's Dirichlet problem, C3):
+// 7 caps them at 72 registers (C3 263.9 -> 254.9 ms on one box; 8 blocks at
+// 64 registers spill: 267.9 ms; 1 lets ptxas take 92 registers: 260.4 ms).
+// The Fourier-velocity walkers need their registers (they spill at 72) and
+// stay unconstrained.
+#ifndef SMC_BVP_MINB
+#define SMC_BVP_MINB 7
+#endif
 
 __device__ __forceinline__ double log_u(double x) { return fm::log_tab(x); }  // uniform in (0,1)
 __device__ __forceinline__ float log_u(float x) { return __logf(x); }
@@ -105,7 +114,8 @@ struct Forcing {
 // staged in shared memory, instead of the runtime-tiled lattice loop.
 // DOM: 1 = box domain compiled in (domain_contains<T, 1>), 0 = any kind.
 template <class T, bool STRICT, int KCAP, int NB = 0, int VEL = 0, bool BASIS = false, int DISK_K = 0, int DOM = 0>
-__global__ void __launch_bounds__(kBvpBlock) bvp_walkers(const BvpLaunch L) {
+__global__ void __launch_bounds__(kBvpBlock, (VEL == 1 && DISK_K == 0 && !STRICT) ? SMC_BVP_MINB : 1)
+    bvp_walkers(const BvpLaunch L) {
     constexpr unsigned FULL = 0xffffffffu;
     __shared__ __align__(16) T disk_coef[DISK_K > 0 ? DiskShape<DISK_K>::n_coef : 2];
     if constexpr (DISK_K > 0) {
