@@ -18,6 +18,8 @@
 // bvp_strict.cu (-fmad=false; the reference's operation order).
 #pragma once
 
+#include <type_traits>
+
 #include "kernels.h"
 #include "scalar_eval.cuh"
 #include "smc_device.cuh"
@@ -27,6 +29,11 @@
 namespace smc {
 
 constexpr int kBvpBlock = 128;
+// Walker steps per run between queue refills (see the run loop below).
+#ifndef SMC_BVP_RUN
+#define SMC_BVP_RUN 8
+#endif
+constexpr int kBvpRun = SMC_BVP_RUN;
 // Minimum resident walker blocks per SM the register allocation must allow,
 // for the constant-velocity walkers (the paper's Dirichlet problem, C3):
 // 7 caps them at 72 registers (C3 263.9 -> 254.9 ms on one box; 8 blocks at
@@ -44,12 +51,16 @@ __device__ __forceinline__ float sqrt_u(float v) { return sqrtf(v); }
 
 // Forcing f(x) evaluated every step.  NB > 0: a Gaussian-bump sum of exactly
 // NB terms held in registers for the whole walk (no per-step loads or
-// dispatch); NB == 0: the generic ScalarField evaluator.
-template <int NB>
+// dispatch); NB == 0: the generic ScalarField evaluator.  FAST (FP64 value
+// walkers): the bump exponentials by fm::exp_bump from the 2 KB table `tab`
+// staged in shared memory — valid only for arguments in [-708, 0], which
+// launch_bvp_walkers proves for the domain before it selects NB > 0.
+template <int NB, bool FAST = false>
 struct Forcing {
     double c1[NB > 0 ? NB : 1], c2[NB > 0 ? NB : 1], amp[NB > 0 ? NB : 1];
     double neg_a = 0.0;
-    __device__ __forceinline__ explicit Forcing(const ScalarImg& f) {
+    const double* tab = nullptr;
+    __device__ __forceinline__ explicit Forcing(const ScalarImg& f, const double* exp_tab = nullptr) : tab(exp_tab) {
         if constexpr (NB > 0) {
             neg_a = f.neg_sharpness;
 #pragma unroll
@@ -96,7 +107,8 @@ struct Forcing {
 #pragma unroll
             for (int i = 0; i < NB; ++i) {
                 const double d1 = x1 - c1[i], d2 = x2 - c2[i];
-                s += amp[i] * SMC_SCALAR_EXP(neg_a * (d1 * d1 + d2 * d2));
+                if constexpr (FAST) s += amp[i] * fm::exp_bump(neg_a * (d1 * d1 + d2 * d2), tab);
+                else s += amp[i] * SMC_SCALAR_EXP(neg_a * (d1 * d1 + d2 * d2));
             }
             return s;
         }
@@ -122,6 +134,12 @@ __global__ void __launch_bounds__(kBvpBlock, (VEL == 1 && DISK_K == 0 && !STRICT
         for (int i = threadIdx.x; i < DiskShape<DISK_K>::n_coef; i += blockDim.x) disk_coef[i] = T(L.disk_coef[i]);
         __syncthreads();
     }
+    constexpr bool kFastBump = NB > 0 && !STRICT && !BASIS && std::is_same<T, double>::value;
+    __shared__ __align__(16) double exp_tab[kFastBump ? 256 : 1];
+    if constexpr (kFastBump) {
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) exp_tab[i] = fm::g_exptab[i];
+        __syncthreads();
+    }
     const disk::SmemCoef<T> dc{static_cast<uint32_t>(__cvta_generic_to_shared(disk_coef))};
     const int lane = threadIdx.x & 31;
     const unsigned long long total = static_cast<unsigned long long>(L.n_obs) * L.n_particles;
@@ -136,7 +154,7 @@ __global__ void __launch_bounds__(kBvpBlock, (VEL == 1 && DISK_K == 0 && !STRICT
     double I[NB > 0 ? NB : 1];
     unsigned long long my_steps = 0;
     cd p1[STRICT ? KCAP + 1 : 1], p2[STRICT ? KCAP + 1 : 1];
-    const Forcing<NB> forcing(L.forcing);
+    const Forcing<NB, kFastBump> forcing(L.forcing, exp_tab);
 
     for (;;) {
         if (!exhausted) {
@@ -168,64 +186,77 @@ __global__ void __launch_bounds__(kBvpBlock, (VEL == 1 && DISK_K == 0 && !STRICT
             }
         }
         if (!__any_sync(FULL, active)) break;
-        if (active) {
-            const Uniform2 u = uniform_block(L.rk, L.obs_slot0 + obs, particle, static_cast<uint64_t>(step));
-            T xi1, xi2, v1, v2;
-            if constexpr (STRICT) {
-                const double r = sqrt(-2.0 * log(u.u0));
-                const double a = 2.0 * kPi * u.u1;
-                xi1 = r * cos(a);
-                xi2 = r * sin(a);
-                velocity_strict<KCAP>(L.vel, p1, p2, x1, x2, v1, v2);
-            } else {
-                const T rad = sqrt_u(T(-2) * log_u(T(u.u0)));
-                T sn, cs;
-                sincospi_t(T(2) * T(u.u1), &sn, &cs);
-                xi1 = rad * cs;
-                xi2 = rad * sn;
-                if (VEL == 1 || L.vel.is_constant) {
-                    v1 = T(L.vel.c1);
-                    v2 = T(L.vel.c2);
-                } else if constexpr (VEL == 0 && DISK_K > 0) {
-                    const T xa[1] = {x1}, xb[1] = {x2};
-                    T va[1], vb[1];
-                    disk::velocity_disk<DISK_K, T, 1>(dc, xa, xb, va, vb);
-                    v1 = va[0];
-                    v2 = vb[0];
-                } else if constexpr (VEL == 0) {
-                    velocity_lattice<T, double>(lat, lat.coef, x1, x2, v1, v2);
-                }
-            }
-            T n1, n2;
-            if constexpr (STRICT) {
-                n1 = x1 - v1 * L.dt + L.sigma * L.root_dt * xi1;
-                n2 = x2 - v2 * L.dt + L.sigma * L.root_dt * xi2;
-            } else {
-                n1 = fma(sr, xi1, fma(-v1, dt, x1));
-                n2 = fma(sr, xi2, fma(-v2, dt, x2));
-            }
-            T f = T(0);
-            double phi[NB > 0 ? NB : 1];
-            if constexpr (BASIS) forcing.basis(double(x1), double(x2), phi);
-            else f = forcing(L.forcing, x1, x2);  // FP64, or the float variant for T = float
-            ++my_steps;
-            if (!domain_contains<T, DOM>(L.domain, n1, n2)) {
-                T h1, h2;
-                const T frac = boundary_exit<T>(L.domain, x1, x2, n1, n2, h1, h2);
-                const T tau = T(double(step)) * dt + frac * dt;
-                if constexpr (BASIS) {
-                    const unsigned long long nw = total;
-#pragma unroll
-                    for (int q = 0; q < NB; ++q) L.basis[q * nw + w] = I[q] + phi[q] * double(frac) * double(dt);
-                    L.values[w] = scalar_eval(L.boundary, double(h1), double(h2));
+        if (!active) continue;
+        // up to kBvpRun steps between refills: the refill vote, the loop-carried
+        // moves and the max_steps test are paid once per run, not per step (a
+        // lane whose walker exits idles for the rest of the run: (kBvpRun - 1)/2
+        // steps per walker against ~800 on C3).  max_steps is hit exactly.
+        {
+            const int64_t left = L.max_steps - step;
+            const int n_run = left < kBvpRun ? static_cast<int>(left) : kBvpRun;
+            int run = 0;
+            // (not unrolled: two steps per iteration lose the uniform-register
+            // constants to per-thread LDC and spill)
+#pragma unroll 1
+            for (; run < n_run; ++run) {
+                const Uniform2 u = uniform_block(L.rk, L.obs_slot0 + obs, particle, static_cast<uint64_t>(step));
+                T xi1, xi2, v1, v2;
+                if constexpr (STRICT) {
+                    const double r = sqrt(-2.0 * log(u.u0));
+                    const double a = 2.0 * kPi * u.u1;
+                    xi1 = r * cos(a);
+                    xi2 = r * sin(a);
+                    velocity_strict<KCAP>(L.vel, p1, p2, x1, x2, v1, v2);
                 } else {
-                    f_int += f * frac * dt;
-                    L.values[w] = scalar_eval(L.boundary, double(h1), double(h2)) - double(f_int);
+                    const T rad = sqrt_u(T(-2) * log_u(T(u.u0)));
+                    T sn, cs;
+                    sincospi_t(T(2) * T(u.u1), &sn, &cs);
+                    xi1 = rad * cs;
+                    xi2 = rad * sn;
+                    if (VEL == 1 || L.vel.is_constant) {
+                        v1 = T(L.vel.c1);
+                        v2 = T(L.vel.c2);
+                    } else if constexpr (VEL == 0 && DISK_K > 0) {
+                        const T xa[1] = {x1}, xb[1] = {x2};
+                        T va[1], vb[1];
+                        disk::velocity_disk<DISK_K, T, 1>(dc, xa, xb, va, vb);
+                        v1 = va[0];
+                        v2 = vb[0];
+                    } else if constexpr (VEL == 0) {
+                        velocity_lattice<T, double>(lat, lat.coef, x1, x2, v1, v2);
+                    }
                 }
-                L.aux[w] = double(tau);
-                L.failed[w] = 0;
-                active = false;
-            } else {
+                T n1, n2;
+                if constexpr (STRICT) {
+                    n1 = x1 - v1 * L.dt + L.sigma * L.root_dt * xi1;
+                    n2 = x2 - v2 * L.dt + L.sigma * L.root_dt * xi2;
+                } else {
+                    n1 = fma(sr, xi1, fma(-v1, dt, x1));
+                    n2 = fma(sr, xi2, fma(-v2, dt, x2));
+                }
+                T f = T(0);
+                double phi[NB > 0 ? NB : 1];
+                if constexpr (BASIS) forcing.basis(double(x1), double(x2), phi);
+                else f = forcing(L.forcing, x1, x2);  // FP64, or the float variant for T = float
+                if (!domain_contains<T, DOM>(L.domain, n1, n2)) {
+                    T h1, h2;
+                    const T frac = boundary_exit<T>(L.domain, x1, x2, n1, n2, h1, h2);
+                    const T tau = T(double(step)) * dt + frac * dt;
+                    if constexpr (BASIS) {
+                        const unsigned long long nw = total;
+#pragma unroll
+                        for (int q = 0; q < NB; ++q) L.basis[q * nw + w] = I[q] + phi[q] * double(frac) * double(dt);
+                        L.values[w] = scalar_eval(L.boundary, double(h1), double(h2));
+                    } else {
+                        f_int += f * frac * dt;
+                        L.values[w] = scalar_eval(L.boundary, double(h1), double(h2)) - double(f_int);
+                    }
+                    L.aux[w] = double(tau);
+                    L.failed[w] = 0;
+                    active = false;
+                    ++run;
+                    break;
+                }
                 if constexpr (BASIS) {
 #pragma unroll
                     for (int q = 0; q < NB; ++q) I[q] += phi[q] * double(dt);
@@ -235,17 +266,18 @@ __global__ void __launch_bounds__(kBvpBlock, (VEL == 1 && DISK_K == 0 && !STRICT
                 x1 = n1;
                 x2 = n2;
                 ++step;
-                if (step >= L.max_steps) {
-                    L.values[w] = 0.0;
-                    L.aux[w] = 0.0;
-                    L.failed[w] = 1;
-                    if constexpr (BASIS) {
-#pragma unroll
-                        for (int q = 0; q < NB; ++q) L.basis[q * total + w] = 0.0;
-                    }
-                    active = false;
-                }
             }
+            my_steps += static_cast<unsigned>(run);
+        }
+        if (active && step >= L.max_steps) {
+            L.values[w] = 0.0;
+            L.aux[w] = 0.0;
+            L.failed[w] = 1;
+            if constexpr (BASIS) {
+#pragma unroll
+                for (int q = 0; q < NB; ++q) L.basis[q * total + w] = 0.0;
+            }
+            active = false;
         }
     }
     // one atomic per warp for the walker-step count

@@ -53,7 +53,11 @@ cudaError_t launch_bvp_walkers(const BvpLaunch& L0, int n_sms, cudaStream_t s) {
     // Gaussian-bump forcing with 1..4 terms (the paper's control problem has 3)
     // keeps its parameters in registers; a constant velocity compiles the
     // Fourier series out.
-    const int nb = (L.forcing.kind == SMC_SCALAR_BUMPS && L.forcing.n >= 1 && L.forcing.n <= 4) ? L.forcing.n : 0;
+    // The FP64 register-resident bumps use the table exponential, valid for
+    // exponents in [-708, 0] only: without that proof (prepare_bvp) they take
+    // the generic evaluator.
+    int nb = (L.forcing.kind == SMC_SCALAR_BUMPS && L.forcing.n >= 1 && L.forcing.n <= 4) ? L.forcing.n : 0;
+    if (L.precision != SMC_FP32 && !L.bump_exp_ok) nb = 0;
     if (L.disk_K > 0 && L.precision == SMC_FP64 && !L.vel.is_constant) return launch_bvp_disk(L, blocks, s);
     if (L.precision == SMC_FP32) dispatch<float>(L, nb, blocks, s);
     else dispatch<double>(L, nb, blocks, s);

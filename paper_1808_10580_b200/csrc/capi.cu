@@ -374,6 +374,37 @@ void ad_observe_range(smc_ctx* ctx, const smc_ad_problem& p, uint64_t seed, int6
     ctx->stats = total;
 }
 
+// True when every Gaussian-bump exponent -a |x - c_j|^2 the walkers can form
+// lies in [-700, 0] (fm::exp_bump's domain, with margin): a >= 0 and a times
+// the largest squared distance from any bump centre to the bounding box of
+// the domain and the launched observation points is at most 700.  Walkers
+// only ever sit at their start point or at an accepted step inside the domain.
+static bool bump_exp_range_ok(const smc_bvp_problem& p, int64_t obs_begin, int64_t obs_count) {
+    const smc_scalar_field& f = p.forcing;
+    if (f.kind != SMC_SCALAR_BUMPS || f.n_terms < 1 || f.center == nullptr) return false;
+    double lo[2], hi[2];
+    if (p.domain.kind == 1) {
+        for (int a = 0; a < 2; ++a) lo[a] = p.domain.lower[a], hi[a] = p.domain.upper[a];
+    } else if (p.domain.kind == 2) {
+        for (int a = 0; a < 2; ++a) lo[a] = p.domain.center[a] - p.domain.radius, hi[a] = p.domain.center[a] + p.domain.radius;
+    } else {
+        return false;
+    }
+    for (int64_t o = obs_begin; o < obs_begin + obs_count; ++o)
+        for (int a = 0; a < 2; ++a) lo[a] = std::min(lo[a], p.obs_x[2 * o + a]), hi[a] = std::max(hi[a], p.obs_x[2 * o + a]);
+    if (!(f.sharpness >= 0.0)) return false;
+    for (int j = 0; j < f.n_terms; ++j) {
+        double d2 = 0.0;
+        for (int a = 0; a < 2; ++a) {
+            const double c = f.center[2 * j + a];
+            const double m = std::max(std::fabs(lo[a] - c), std::fabs(hi[a] - c));
+            d2 += m * m;
+        }
+        if (!(f.sharpness * d2 <= 700.0)) return false;
+    }
+    return true;
+}
+
 BvpLaunch prepare_bvp(smc_ctx* ctx, const smc_bvp_problem& p, int64_t obs_begin, int64_t obs_count) {
     const PreparedVelocity v = prepare_velocity(p.velocity);
     check_kappa(p.kappa);
@@ -426,6 +457,7 @@ BvpLaunch prepare_bvp(smc_ctx* ctx, const smc_bvp_problem& p, int64_t obs_begin,
     L.root_dt = std::sqrt(dt);
     L.sr = L.sigma * L.root_dt;
     L.precision = p.precision;
+    L.bump_exp_ok = bump_exp_range_ok(p, obs_begin, obs_count) ? 1 : 0;
     return L;
 }
 

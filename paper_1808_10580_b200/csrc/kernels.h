@@ -77,7 +77,7 @@ struct BvpLaunch {
     int64_t max_steps;
     double dt, root_dt, sigma, sr;  // sr = sigma * sqrt(dt)
     int32_t precision;
-    int32_t pad_;
+    int32_t bump_exp_ok;       // every bump exponent provably in [-708, 0] (fm::exp_bump valid; prepare_bvp)
     unsigned long long* counter;     // walker queue head (zeroed before launch)
     unsigned long long* step_total;  // total walker-steps executed (atomicAdd)
     double* values;            // [n_obs][n_particles]

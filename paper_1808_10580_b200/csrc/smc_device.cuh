@@ -76,8 +76,9 @@ SMC_HD u32x4 philox4x32_10(u32x4 c, const RoundKeys& rk) {
 SMC_HD double u53_to_unit(uint64_t word) {
     const uint64_t m = word >> 11;
 #ifdef __CUDA_ARCH__
-    const double dm = __ull2double_rn(m);
-    return __dmul_rn(__dadd_rn(dm, 0.5), 0x1p-53);
+    // one rounding of (m + 1/2) 2^-53, as the reference's RN(m + 0.5) scaled
+    // exactly by 2^-53: one DFMA instead of DADD + DMUL
+    return __fma_rn(__ull2double_rn(m), 0x1p-53, 0x1p-54);
 #else
     return (static_cast<double>(m) + 0.5) * 0x1p-53;
 #endif

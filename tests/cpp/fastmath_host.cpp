@@ -17,6 +17,9 @@ void fm_log_tab(const double* x, int64_t n, double* y) {
 void fm_exp(const double* x, int64_t n, double* y) {
     for (int64_t i = 0; i < n; ++i) y[i] = smc::fm::exp_(x[i]);
 }
+void fm_exp_bump(const double* x, int64_t n, double* y) {
+    for (int64_t i = 0; i < n; ++i) y[i] = smc::fm::exp_bump(x[i], smc::fm::h_exptab);
+}
 void fm_sqrt(const double* x, int64_t n, double* y) {
     for (int64_t i = 0; i < n; ++i) y[i] = smc::fm::sqrt_pos(x[i]);
 }

@@ -22,7 +22,7 @@ def fm(tmp_path_factory):
                     str(ROOT / "tests/cpp/fastmath_host.cpp")], check=True)
     lib = C.CDLL(str(out))
     P = C.POINTER(C.c_double)
-    for name, n in [("fm_sincospi", 4), ("fm_log", 3), ("fm_log_tab", 3), ("fm_exp", 3), ("fm_sqrt", 3),
+    for name, n in [("fm_sincospi", 4), ("fm_log", 3), ("fm_log_tab", 3), ("fm_exp", 3), ("fm_exp_bump", 3), ("fm_sqrt", 3),
                     ("fm_div", 4)]:
         getattr(lib, name).restype = None
     return lib
@@ -107,6 +107,17 @@ def test_exp(fm):
     fm.fm_exp(_p(z), C.c_int64(z.size), _p(w))
     assert np.isinf(w[0]) and np.isinf(w[1]) and w[2] == 0.0
     assert ulp_err(w[3:], [mpmath.exp(mpmath.mpf(v)) for v in z[3:]]) <= 2.0
+
+
+def test_exp_bump(fm):
+    """fm::exp_bump, the walkers' table exponential, on its whole domain [-708, 0]
+    (the launcher proves the bump exponents lie in [-700, 0])."""
+    x = np.concatenate([RNG.uniform(-708, 0, 3000), RNG.uniform(-1, 0, 1000), -RNG.uniform(0, 1e-3, 500),
+                        [0.0, -0.0, -1e-300, -708.0, -700.0, -np.log(2) / 512, -np.log(2) / 256]])
+    y = np.empty_like(x)
+    fm.fm_exp_bump(_p(x), C.c_int64(x.size), _p(y))
+    assert ulp_err(y, [mpmath.exp(mpmath.mpf(v)) for v in x]) <= 1.5
+    assert y[-7] == 1.0 and y[-6] == 1.0 and y[-5] == 1.0
 
 
 def test_sqrt_and_div_correctly_rounded(fm):
