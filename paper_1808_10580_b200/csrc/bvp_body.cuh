@@ -29,23 +29,27 @@
 namespace smc {
 
 constexpr int kBvpBlock = 128;
-// Walker steps per run between queue refills (see the run loop below).
+// Walker steps per run between queue refills (see the run loop below;
+// C3: 4 -> 226.2, 8 -> 222.4, 16 -> 219.7, 32 -> 219.1 ms, same box).
 #ifndef SMC_BVP_RUN
-#define SMC_BVP_RUN 8
+#define SMC_BVP_RUN 16
 #endif
 constexpr int kBvpRun = SMC_BVP_RUN;
 // Minimum resident walker blocks per SM the register allocation must allow,
-// for the constant-velocity walkers (the paper's Dirichlet problem, C3):
-// 7 caps them at 72 registers (C3 263.9 -> 254.9 ms on one box; 8 blocks at
-// 64 registers spill: 267.9 ms; 1 lets ptxas take 92 registers: 260.4 ms).
-// The Fourier-velocity walkers need their registers (they spill at 72) and
-// stay unconstrained.
+// for the constant-velocity walkers (the paper's Dirichlet problem, C3).
+// Before the run loop and the table exponential, 7 (72 registers) was best
+// (C3 263.9 -> 254.9 ms on one box; 8 blocks at 64 registers spilled in the
+// step: 267.9 ms).  With the shorter step, 8 blocks at 64 registers (a few
+// spill loads per step) beat 7 blocks at 72: 219.7 -> 218.0 ms
+// (profiles/r02_ab_k2_expbump_runloop.log).  The Fourier-velocity walkers
+// need their registers (they spill at 72) and stay unconstrained.
 #ifndef SMC_BVP_MINB
-#define SMC_BVP_MINB 7
+#define SMC_BVP_MINB 8
 #endif
 
-__device__ __forceinline__ double log_u(double x) { return fm::log_tab(x); }  // uniform in (0,1)
-__device__ __forceinline__ float log_u(float x) { return __logf(x); }
+// uniform in (0,1); FP64 from the log table staged in shared memory
+__device__ __forceinline__ double log_u(double x, const double* tab) { return fm::log_tab(x, tab); }
+__device__ __forceinline__ float log_u(float x, const double*) { return __logf(x); }
 __device__ __forceinline__ double sqrt_u(double v) { return fm::sqrt_pos(v); }
 __device__ __forceinline__ float sqrt_u(float v) { return sqrtf(v); }
 
@@ -134,6 +138,14 @@ __global__ void __launch_bounds__(kBvpBlock, (VEL == 1 && DISK_K == 0 && !STRICT
         for (int i = threadIdx.x; i < DiskShape<DISK_K>::n_coef; i += blockDim.x) disk_coef[i] = T(L.disk_coef[i]);
         __syncthreads();
     }
+    // shared-memory copies of the log table (FP64 Box-Muller: 32-bit LDS
+    // addressing instead of 64-bit global) and of exp_bump's table
+    constexpr bool kLogTab = !STRICT && std::is_same<T, double>::value;
+    __shared__ __align__(16) double log_tab[kLogTab ? 512 : 2];
+    if constexpr (kLogTab) {
+        for (int i = threadIdx.x; i < 512; i += blockDim.x) log_tab[i] = fm::g_logtab[i];
+        __syncthreads();
+    }
     constexpr bool kFastBump = NB > 0 && !STRICT && !BASIS && std::is_same<T, double>::value;
     __shared__ __align__(16) double exp_tab[kFastBump ? 256 : 1];
     if constexpr (kFastBump) {
@@ -208,9 +220,9 @@ __global__ void __launch_bounds__(kBvpBlock, (VEL == 1 && DISK_K == 0 && !STRICT
                     xi2 = r * sin(a);
                     velocity_strict<KCAP>(L.vel, p1, p2, x1, x2, v1, v2);
                 } else {
-                    const T rad = sqrt_u(T(-2) * log_u(T(u.u0)));
+                    const T rad = sqrt_u(T(-2) * log_u(T(u.u0), log_tab));
                     T sn, cs;
-                    sincospi_t(T(2) * T(u.u1), &sn, &cs);
+                    sincospi_shift(T(2) * T(u.u1), &sn, &cs);
                     xi1 = rad * cs;
                     xi2 = rad * sn;
                     if (VEL == 1 || L.vel.is_constant) {

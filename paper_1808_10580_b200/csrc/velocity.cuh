@@ -32,6 +32,9 @@ __device__ __forceinline__ void sincospi_t(float a, float* s, float* c) {
     const float r = fmaf(-2.0f, rintf(0.5f * a), a);  // a - 2 round(a / 2), exact
     __sincosf(3.14159265f * r, s, c);
 }
+// the quadrant by FP64 adds instead of FRND/F2I (issue-bound walker kernels)
+__device__ __forceinline__ void sincospi_shift(double a, double* s, double* c) { fm::sincospi<true>(a, s, c); }
+__device__ __forceinline__ void sincospi_shift(float a, float* s, float* c) { sincospi_t(a, s, c); }
 
 // Four coefficients (alpha_re, alpha_im, beta_re, beta_im) of one pair.
 template <class T>

@@ -8,6 +8,9 @@ extern "C" {
 void fm_sincospi(const double* a, int64_t n, double* s, double* c) {
     for (int64_t i = 0; i < n; ++i) smc::fm::sincospi(a[i], s + i, c + i);
 }
+void fm_sincospi_shift(const double* a, int64_t n, double* s, double* c) {
+    for (int64_t i = 0; i < n; ++i) smc::fm::sincospi<true>(a[i], s + i, c + i);
+}
 void fm_log(const double* x, int64_t n, double* y) {
     for (int64_t i = 0; i < n; ++i) y[i] = smc::fm::log_pos(x[i]);
 }

@@ -22,7 +22,7 @@ def fm(tmp_path_factory):
                     str(ROOT / "tests/cpp/fastmath_host.cpp")], check=True)
     lib = C.CDLL(str(out))
     P = C.POINTER(C.c_double)
-    for name, n in [("fm_sincospi", 4), ("fm_log", 3), ("fm_log_tab", 3), ("fm_exp", 3), ("fm_exp_bump", 3), ("fm_sqrt", 3),
+    for name, n in [("fm_sincospi", 4), ("fm_sincospi_shift", 4), ("fm_log", 3), ("fm_log_tab", 3), ("fm_exp", 3), ("fm_exp_bump", 3), ("fm_sqrt", 3),
                     ("fm_div", 4)]:
         getattr(lib, name).restype = None
     return lib
@@ -107,6 +107,18 @@ def test_exp(fm):
     fm.fm_exp(_p(z), C.c_int64(z.size), _p(w))
     assert np.isinf(w[0]) and np.isinf(w[1]) and w[2] == 0.0
     assert ulp_err(w[3:], [mpmath.exp(mpmath.mpf(v)) for v in z[3:]]) <= 2.0
+
+
+def test_sincospi_shift_quadrant_identical(fm):
+    """sincospi<true> (quadrant from the 1.5 2^52 shifter, the walkers) equals
+    sincospi<false> (rint) bit for bit, ties and quarter turns included."""
+    a = np.concatenate([RNG.uniform(-4, 4, 4000), RNG.uniform(0, 2, 2000), np.arange(-16, 17) * 0.125,
+                        np.arange(-8, 9) * 0.25 + 2.0 ** -40, [1e6 + 0.25, -3e9 + 0.75, 0.0, -0.0]])
+    s0, c0, s1, c1 = (np.empty_like(a) for _ in range(4))
+    fm.fm_sincospi(_p(a), C.c_int64(a.size), _p(s0), _p(c0))
+    fm.fm_sincospi_shift(_p(a), C.c_int64(a.size), _p(s1), _p(c1))
+    assert np.array_equal(s0.view(np.uint64), s1.view(np.uint64))
+    assert np.array_equal(c0.view(np.uint64), c1.view(np.uint64))
 
 
 def test_exp_bump(fm):
