@@ -414,7 +414,10 @@ __device__ __forceinline__ void velocity_disk(const CA& C, const T (&x1)[P], con
 // rejected: unrolling every row (instruction-fetch bound, C4 2969 vs 2763
 // ms) and interleaving the pair updates of two rows (eight accumulator
 // chains instead of four: 2974 -> 3032 ms).
-constexpr int kDiskTile = 8;
+#ifndef SMC_DISK_TILE
+#define SMC_DISK_TILE 8
+#endif
+constexpr int kDiskTile = SMC_DISK_TILE;
 
 template <int K, int T0>
 struct DiskTile {
