@@ -74,12 +74,13 @@ SMC_HD u32x4 philox4x32_10(u32x4 c, const RoundKeys& rk) {
 // 53 random bits into (0,1): ((m) + 0.5) * 2^-53 with IEEE rounding of the
 // add — bit-identical to rng.cpp:59-64.  m < 2^53, so the conversion is exact.
 SMC_HD double u53_to_unit(uint64_t word) {
-    const uint64_t m = word >> 11;
 #ifdef __CUDA_ARCH__
-    // one rounding of (m + 1/2) 2^-53, as the reference's RN(m + 0.5) scaled
-    // exactly by 2^-53: one DFMA instead of DADD + DMUL
-    return __fma_rn(__ull2double_rn(m), 0x1p-53, 0x1p-54);
+    // the conversion of the 54-bit odd integer 2m + 1 is the one rounding of
+    // the reference's RN(m + 0.5) (scaled by 2), and the power-of-two scale is
+    // exact: I2F + DMUL by an immediate, no DADD and no constant registers
+    return __dmul_rn(__ull2double_rn((word >> 10) | 1ull), 0x1p-54);
 #else
+    const uint64_t m = word >> 11;
     return (static_cast<double>(m) + 0.5) * 0x1p-53;
 #endif
 }
