@@ -345,7 +345,10 @@ def run_ours(args):
         sb, se = D.sample_range(len(U), rank, world)
         h2d, d2h = U[sb:se].nbytes + 2048, 40 * len(base.observations) * len(U)
         api = "paper_1808_10580_b200.observe_ad_batched -> smc_ad_observe_batched (C ABI)"
-        kernel_name = "ad_particles<double> generic tiled lattice (K1)"
+        # FP64 K = 25 prior (C4): the compile-time tiled disk kernel; the FP32
+        # variant keeps the generic tiled lattice kernel
+        kernel_name = ("ad_particles<float> generic tiled lattice (K1)" if fp32
+                       else "ad_particles_disk<25> tiled disk (K1)")
         shard = "parameter samples"
     if world > 1:
         g = ctx.group()
