@@ -612,3 +612,19 @@ def test_k25_dense_field_paths(ctx, port, monkeypatch):
     lattice = S.observe_ad(spec, 808, ctx=ctx)
     for a, b in zip(lattice, disk):
         assert abs(a.mean - b.mean) <= 1e-12 and abs(a.std_error - b.std_error) <= 1e-10 * b.std_error
+
+
+@pytest.mark.parametrize("sharpness", [4.0, 150.0, 2000.0])
+def test_bvp_bump_exponent_range_paths(ctx, port, sharpness):
+    """The walkers' table exponential (fm::exp_bump) is valid for exponents in
+    [-708, 0]; prepare_bvp proves -a|x - c|^2 >= -700 over the domain's
+    bounding box (a = 4 and 150: proved, table path) or falls back to the
+    generic evaluator (a = 2000: max a d^2 ~ 1600).  Both match the oracle."""
+    centers = [(0.68, 0.4), (0.4, 0.68), (0.82, 0.82)]
+    spec = specs.c3_spec(n_particles=600)
+    spec.observations = [(0.7, 0.42), (0.5, 0.5), (0.83, 0.8)]
+    spec.forcing = S.ScalarField.gaussian_bumps(
+        [S.Bump(a, S.Vec2(*c)) for a, c in zip((1.0, -0.5, 2.0), centers)], sharpness)
+    got = S.observe_bvp(spec, 606, ctx=ctx)
+    want = port.observe_bvp(spec, 606)
+    assert_estimates(got, list(want), 1.0)
