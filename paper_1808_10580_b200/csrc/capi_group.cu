@@ -518,6 +518,14 @@ smc_status smc_create_multi(int ndev, const int* devs, smc_ctx** out) {
                     }
                 }
             }
+            // Modelling knob (emulated groups on one GPU): SMC_GROUP_SERIAL=1
+            // puts every member on the lead's stream, so the members' shards
+            // run one after another and each member's particle-kernel time is
+            // what one rank of a W-GPU group would see (tools/shard_model.py)
+            const char* serial = std::getenv("SMC_GROUP_SERIAL");
+            if (!api && serial && std::atoi(serial) == 1)
+                for (int i = 1; i < ndev; ++i)
+                    if (devs[i] == devs[0]) g->members[i]->stream = lead->stream;
             CK(cudaSetDevice(devs[0]));
         } catch (...) {
             smc_destroy(lead);
