@@ -750,7 +750,7 @@ static void reduce_bvp(smc_ctx* ctx, const double* values, const double* aux, co
     count_launches(ctx, launches + 2);
     smc_estimate* h = ctx->est_host.get<smc_estimate>(static_cast<size_t>(n_obs));
     CK(cudaMemcpyAsync(h, est, sizeof(smc_estimate) * n_obs, cudaMemcpyDeviceToHost, s));
-    unsigned long long* steps_h = ctx->staging.get<unsigned long long>(1);
+    unsigned long long* steps_h = ctx->steps_host.get<unsigned long long>(1);
     *steps_h = 0;
     if (step_total)
         CK(cudaMemcpyAsync(steps_h, step_total, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));

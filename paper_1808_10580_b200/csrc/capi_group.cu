@@ -429,7 +429,7 @@ void group_bvp_observe(smc_ctx* ctx, const smc_bvp_problem& p, uint64_t seed, in
         smc_estimate* est = c->est.get<smc_estimate>(static_cast<size_t>(no));
         CK(launch_estimates(means[m], sums[m] + 2 * no, sums[m] + no, nvalid[m], n, n, no, est, c->stream));
         count_launches(c, 2);
-        unsigned long long* sh = c->staging.get<unsigned long long>(1);
+        unsigned long long* sh = c->steps_host.get<unsigned long long>(1);
         *sh = 0;
         if (steps[m]) CK(cudaMemcpyAsync(sh, steps[m], sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
         if (m == 0) {
@@ -447,7 +447,7 @@ void group_bvp_observe(smc_ctx* ctx, const smc_bvp_problem& p, uint64_t seed, in
         agg.particle_kernel_ms = std::max(agg.particle_kernel_ms, c->stats.particle_kernel_ms);
         agg.reduce_ms = std::max(agg.reduce_ms, c->stats.reduce_ms);
         agg.kernel_launches += c->stats.kernel_launches;
-        agg.particle_steps += static_cast<int64_t>(*c->staging.get<unsigned long long>(1));
+        agg.particle_steps += static_cast<int64_t>(*c->steps_host.get<unsigned long long>(1));
     }
     CK(cudaSetDevice(ctx->device));
     ctx->stats = agg;

@@ -186,7 +186,11 @@ struct smc_ctx {
     DevBuf gx_a, gx_b, gx_c, gx_d;  // group exchange buffers (every rank's contribution)
     DevBuf pk_ip, pk_im, pk_kp, pk_km, pk_ms, pk_u, pk_blocks, pk_bad;  // device u -> field packing
     DevBuf gal_A, gal_t0, gal_t1, gal_k1, gal_k2, gal_obs, gal_grid;  // Galerkin reference solver
-    PinnedBuf staging, est_host;
+    // staging: the problem image's H2D source, read by a copy that may still
+    // be queued behind earlier work on the stream when the call returns to
+    // the host — nothing else may write it before the call's final sync;
+    // steps_host: the walker-step count read back at the end of a call
+    PinnedBuf staging, est_host, steps_host;
     smc_stats stats{};
 
     unsigned char* upload(const Image& img) {

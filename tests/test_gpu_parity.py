@@ -628,3 +628,26 @@ def test_bvp_bump_exponent_range_paths(ctx, port, sharpness):
     got = S.observe_bvp(spec, 606, ctx=ctx)
     want = port.observe_bvp(spec, 606)
     assert_estimates(got, list(want), 1.0)
+
+
+def test_forward_maps_on_a_busy_stream(ctx):
+    """The problem image's H2D copy reads pinned staging memory; when the
+    context's stream is busy (here: a 0.1 s sleep kernel queued ahead, as the
+    bench's L2 flush or a caller's own work can be) that copy is still
+    pending while the host enqueues the rest of the call, so nothing else may
+    write the staging buffer before the call's final sync (the Dirichlet
+    map's walker-step readback once did).  Results equal the idle-stream ones."""
+    import torch
+    busy = S.Context(0)
+    s = torch.cuda.Stream(device=0)
+    S.load_library().smc_set_stream(busy.handle, s.cuda_stream)
+    bvp = specs.paper_bvp(n_particles=3000, amplitudes=(1.0, -0.5, 2.0))
+    ad = specs.c1_two_mode(n_particles=4096)
+    for run in (lambda c: S.observe_bvp(bvp, 606, ctx=c), lambda c: S.observe_ad(ad, 7, ctx=c)):
+        want = run(ctx)
+        with torch.cuda.stream(s):
+            torch.cuda._sleep(200_000_000)
+        got = run(busy)
+        for a, b in zip(got, want):
+            assert (a.mean, a.std_error, a.aux_mean, a.n_particles, a.n_failed) == \
+                (b.mean, b.std_error, b.aux_mean, b.n_particles, b.n_failed)

@@ -25,21 +25,20 @@ os.environ.setdefault("SMC_GROUP_EXCHANGE", "emulated")
 os.environ["SMC_GROUP_SERIAL"] = "1"
 
 import paper_1808_10580_b200 as S  # noqa: E402
-import specs  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--config", default="c2", choices=["c2", "c3"])
+ap.add_argument("--config", default="c2", choices=["c2", "c3", "c5"])
 ap.add_argument("--worlds", default="1,2,4,8")
 ap.add_argument("--reps", type=int, default=3)
 args = ap.parse_args()
 
+import bench  # noqa: E402  (the bench's workloads, same specs and seeds)
+
 base = S.default_context(0)
-if args.config == "c2":
-    u = S.prior_draw(specs.C2_PRIOR, 808, 0xBE9C4, 0, base)
-    spec = specs.c2_spec(u)
+kind, spec, _ = bench.build_workload(args.config, base)
+if kind == "ad":
     run = lambda ctx: S.observe_ad(spec, 808, ctx=ctx)  # noqa: E731
 else:
-    spec = specs.c3_spec()
     run = lambda ctx: S.observe_bvp(spec, 606, ctx=ctx)  # noqa: E731
 
 one = None
