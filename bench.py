@@ -449,7 +449,10 @@ def run_ours(args):
                                        "kernels execute fewer (4 FMA per mode, Chebyshev harmonics), so frac can "
                                        "exceed 1 — `executed` is the hardware figure: the FP64 flops the kernel "
                                        "actually issues per particle-step (ncu) at the same rate",
-                         "executed": executed, "traffic": traffic},
+                         "executed": executed,
+                         # dram bytes per launch of the dominant kernel (ncu --set full capture), or null
+                         "traffic": None if not traffic else traffic.get("dram_bytes_per_launch"),
+                         "traffic_detail": traffic},
             "gpu_launches": launches,
             "clocks": clocks,
         }
