@@ -211,3 +211,19 @@ def test_pcn_group_chain_sharding(ctx, world, chains):
     got = S.run_chains(cfg, prior, like, seeds, ctx=group(world))
     for k in ("final_u", "final_phi", "map_u", "map_objective", "accepted", "phi_trace", "samples"):
         assert np.array_equal(got[k], want[k]), k
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_serialised_group_bit_identical(ctx, monkeypatch, world):
+    """SMC_GROUP_SERIAL=1 (tools/shard_model.py: every member on one stream,
+    so each shard runs alone and its kernel time is one rank's) must not
+    change results: with all members' work queued behind each other, any
+    host write into a buffer an earlier queued copy still reads shows up here
+    (it caught the Dirichlet map's step-count readback into the image's
+    staging buffer)."""
+    monkeypatch.setenv("SMC_GROUP_SERIAL", "1")
+    g = S.Context(devices=[0] * world)
+    ad = ragged_c2(ctx)
+    assert same(S.observe_ad(ad, 808, ctx=g), S.observe_ad(ad, 808, ctx=ctx))
+    bvp = specs.paper_bvp(n_particles=20000, amplitudes=(1.0, -0.5, 2.0))
+    assert same(S.observe_bvp(bvp, 606, ctx=g), S.observe_bvp(bvp, 606, ctx=ctx))
