@@ -1,3 +1,11 @@
+"""Walker-sharded Dirichlet map vs one device at C3 shapes (5e3 / 1e5 / 1e6
+walkers per observation), emulated groups of 2 and 8 members on device 0,
+concurrent (SMC_GROUP_SERIAL=0) and serialised (=1).  Prints the largest
+mean / SE / exit-time differences and any count mismatch; all must be 0.
+(The serialised runs exposed the staging race fixed in round 2.)
+
+    python tools/bvp_shard_check.py
+"""
 import os, sys
 sys.path[:0] = ['.', 'tests']
 os.environ["SMC_GROUP_EXCHANGE"] = "emulated"
