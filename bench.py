@@ -315,7 +315,13 @@ def run_ours(args):
         target = payload[0] if kind == "batched" else payload
         target.precision = S.Precision.fp32
         desc = dict(desc, workload=desc["workload"].replace("FP64", "FP32 variant"), precision="fp32")
+    # the roofline denominator, measured on this GPU now; its clocks are
+    # sampled the same way as the timed region's (roofline.peak_clocks)
+    peak_sampler = ClockSampler(local)
+    peak_sampler.start()
+    time.sleep(0.3)
     peak = ctx.fp32_peak_tflops(300.0) if fp32 else ctx.fp64_peak_tflops(300.0)
+    peak_clocks = peak_sampler.stop()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
 
     if kind == "ad":
@@ -449,6 +455,7 @@ def run_ours(args):
                                        "kernels execute fewer (4 FMA per mode, Chebyshev harmonics), so frac can "
                                        "exceed 1 — `executed` is the hardware figure: the FP64 flops the kernel "
                                        "actually issues per particle-step (ncu) at the same rate",
+                         "peak_clocks": peak_clocks,
                          "executed": executed,
                          # dram bytes per launch of the dominant kernel (ncu --set full capture), or null
                          "traffic": None if not traffic else traffic.get("dram_bytes_per_launch"),
