@@ -26,9 +26,11 @@ namespace {
 
 constexpr int kBlock = 128;
 
-// Resident 128-thread blocks per SM for the tiled disk kernels (K > kDiskMaxK).
+// Resident 128-thread blocks per SM for the tiled disk kernels (K > kDiskMaxK):
+// 3 (168 registers, no spills) beats 4 (128 registers, 80 B of spills) on C4,
+// 2 770 -> 2 709 ms (profiles/r02_ab_c4_tiled_minb.log).
 #ifndef SMC_TILED_MINB
-#define SMC_TILED_MINB 4
+#define SMC_TILED_MINB 3
 #endif
 
 using namespace disk;
